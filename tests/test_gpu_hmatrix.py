@@ -1,0 +1,193 @@
+"""GPU H-matrix assembly vs the reference (golden) and the CPU oracle.
+
+Bars (BASELINE.json north star):
+  * block partition bit-exact (tests/test_abi.py, CPU);
+  * matvec against random vectors within the ACA tolerance of the dense
+    operator (10 eps, as test_acceptance.py:176-191), and within 10 eps of
+    the reference H-matrix matvec (pivots may legitimately diverge);
+  * admissible leaves within 10 eps of the exact block (test_hmatrix.py:257-270);
+  * near-field (dense) leaves equal to the reference entries to 1e-12.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import hbem_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    ("ico2_p0_lap_slp", "p0", "laplace", "slp", 0.0),
+    ("ico2_p0_lap_slp_e5", "p0", "laplace", "slp", 0.0),
+    ("ico2_p0_helm_slp", "p0", "helmholtz", "slp", 2.0),
+    ("ico2_p0_lap_dlp", "p0", "laplace", "dlp", 0.0),
+    ("ico2_p1c_lap_dlp", "p1c", "laplace", "dlp", 0.0),
+]
+
+
+def ico(level):
+    m = golden("meshes")
+    return m[f"ico{level}_vertices"], m[f"ico{level}_elements"]
+
+
+def setup(v, e, fam, eq, op, k, prec="double"):
+    from paper_1711_01897_b200.discretization import OperatorSpec, TriangleMesh, build_space
+    from paper_1711_01897_b200.partition import cluster_trees_for
+    spec = OperatorSpec(eq, op, k, prec)
+    sp = build_space(TriangleMesh(v, e), fam)
+    return spec, sp, cluster_trees_for(sp, sp)
+
+
+@pytest.mark.parametrize("name,fam,eq,op,k", CASES)
+def test_hmatrix_matvec_vs_reference(name, fam, eq, op, k):
+    from paper_1711_01897_b200.hmatrix import AcaConfig, LowRankBlock, assemble_hmatrix
+    g = golden("hmatrices")
+    eps = float(g[f"{name}_eps"][0])
+    v, e = ico(2)
+    spec, sp, bt = setup(v, e, fam, eq, op, k)
+    stats = {}
+    h = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=eps), stats=stats)
+    for x, hx, dx in zip(g[f"{name}_x"], g[f"{name}_hx"], g[f"{name}_dx"]):
+        y = h.matvec(x)
+        assert np.linalg.norm(y - dx) <= 10 * eps * np.linalg.norm(dx)
+        assert np.linalg.norm(y - hx) <= 10 * eps * np.linalg.norm(hx)
+    ranks = np.array([p.rank if isinstance(p, LowRankBlock) else -1 for p in h.payloads])
+    ref_ranks = g[f"{name}_ranks"]
+    # same algorithm, same pivots up to floating-point ties
+    assert (ranks == ref_ranks).mean() >= 0.95, (ranks != ref_ranks).sum()
+    assert stats["lowrank_leaves"] == (ranks >= 0).sum()
+    assert stats["dense_leaves"] == (ranks < 0).sum()
+    if fam == "p0":
+        assert stats["singular_pairs"] == g[f"{name}_counters"][0]
+
+
+def test_dense_leaves_and_admissible_accuracy(rng):
+    """Every admissible leaf within 10 eps of its exact block; every dense
+    near-field leaf equal to the reference dense matrix to 1e-12."""
+    from paper_1711_01897_b200.hmatrix import AcaConfig, DenseBlock, assemble_hmatrix
+    g = golden("hmatrices")
+    dense = g["ico2_p0_lap_slp_dense"]
+    v, e = ico(2)
+    spec, sp, bt = setup(v, e, "p0", "laplace", "slp", 0.0)
+    eps = 1e-5
+    h = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=eps))
+    rp = bt.rows.permutation
+    na = bt.rows.node_array
+    checked = 0
+    for ix, (r, c, adm) in enumerate(bt.leaf_array):
+        blk = dense[np.ix_(rp[na[r, 0]:na[r, 1]], rp[na[c, 0]:na[c, 1]])]
+        got = h.payloads[ix].todense()
+        if adm:
+            assert np.linalg.norm(got - blk) <= 10 * eps * np.linalg.norm(blk)
+            checked += 1
+        else:
+            assert isinstance(h.payloads[ix], DenseBlock)
+            assert np.abs(got - blk).max() <= 1e-12 * np.abs(blk).max()
+    assert checked > 0
+
+
+def test_eta_zero_reproduces_dense():
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix, compression_stats
+    from paper_1711_01897_b200.partition import cluster_trees_for
+    g = golden("hmatrices")
+    dense = g["ico2_p0_lap_slp_dense"]
+    v, e = ico(2)
+    spec, sp, _ = setup(v, e, "p0", "laplace", "slp", 0.0)
+    bt0 = cluster_trees_for(sp, sp, n_min=8, eta=0.0)
+    h0 = assemble_hmatrix(spec, sp, sp, bt0, AcaConfig())
+    assert np.abs(h0.to_dense() - dense).max() <= 1e-12 * np.abs(dense).max()
+    cs = compression_stats(h0)
+    assert cs.ratio == 1.0 and cs.n_lowrank_leaves == 0 and cs.rank_histogram == {}
+
+
+def test_rank_cap_falls_back_to_dense_rows():
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix
+    from paper_1711_01897_b200.partition import cluster_trees_for
+    g = golden("hmatrices")
+    dense = g["ico2_p0_lap_slp_dense"]
+    v, e = ico(2)
+    spec, sp, _ = setup(v, e, "p0", "laplace", "slp", 0.0)
+    bt = cluster_trees_for(sp, sp, n_min=8)
+    stats = {}
+    h = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=1e-14, k_max=1), stats=stats)
+    assert stats["aca_fallback_dense"] > 0
+    assert np.allclose(h.to_dense(), dense, rtol=0, atol=1e-12 * np.abs(dense).max())
+
+
+def test_c1_config_vs_oracle(rng):
+    """C1: Laplace SLP P0, geodesic n=11 (2 420 triangles), eps 1e-3, FP64:
+    GPU H-matrix matvec vs the oracle's H-matrix and vs the exact operator."""
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix, compression_stats
+    from paper_1711_01897_b200.meshes import geodesic_sphere
+    v, e = geodesic_sphere(11)
+    eps = 1e-3
+    spec, sp, bt = setup(v, e, "p0", "laplace", "slp", 0.0)
+    stats = {}
+    h = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=eps), stats=stats)
+    P = O.Problem(O.Spec("laplace", "slp"), v, e)
+    tree = O.cluster_tree(P.dof_centers("p0"), 32)
+    leaves = O.block_tree(tree, tree, 2.0)
+    asm = O.Assembler(P, tree, tree, leaves, eps)
+    ref_payloads = asm.assemble()
+    for _ in range(3):
+        x = rng.standard_normal(len(e))
+        y = h.matvec(x)
+        yr = O.hmat_matvec(tree, tree, leaves, ref_payloads, x)
+        assert np.linalg.norm(y - yr) <= 10 * eps * np.linalg.norm(yr)
+    ranks = np.array([p.rank if hasattr(p, "rank") else -1 for p in h.payloads])
+    ref_ranks = np.array([p.rank if isinstance(p, O.LowRank) else -1 for p in ref_payloads])
+    assert (ranks == ref_ranks).mean() >= 0.95
+    assert stats["singular_pairs"] == asm.counters["singular_pairs"]
+    cs = compression_stats(h)
+    assert cs.ratio < 1.0
+
+
+def test_single_precision_hmatrix():
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix
+    g = golden("hmatrices")
+    v, e = ico(2)
+    spec, sp, bt = setup(v, e, "p0", "laplace", "slp", 0.0, "single")
+    h = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=1e-3))
+    x = g["ico2_p0_lap_slp_x"][0]
+    dx = g["ico2_p0_lap_slp_dx"][0]
+    y = h.matvec(x)
+    assert h.payloads[0].todense().dtype == np.float32
+    assert np.linalg.norm(y - dx) <= 1e-2 * np.linalg.norm(dx)
+
+
+def test_multi_backend_split_bit_identical():
+    """Leaves split across two backends (cost-weighted ranges) give payloads
+    bit-identical to one backend: blocks are independent units."""
+    from paper_1711_01897_b200.backend import make_gpu_backends
+    from paper_1711_01897_b200.discretization import make_integration_context
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix
+    v, e = ico(2)
+    spec, sp, bt = setup(v, e, "p0", "helmholtz", "slp", 2.0)
+    ctx = make_integration_context(spec, sp, sp)
+    one = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=1e-4), make_gpu_backends(ctx, 1))
+    two = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=1e-4), make_gpu_backends(ctx, 2))
+    assert len(two.parts) == 2
+    for p1, p2 in zip(one.payloads, two.payloads):
+        assert type(p1) is type(p2)
+        if hasattr(p1, "u"):
+            assert np.array_equal(p1.u, p2.u) and np.array_equal(p1.v, p2.v)
+        else:
+            assert np.array_equal(p1.a, p2.a)
+
+
+def test_api_errors():
+    from paper_1711_01897_b200.backend import make_gpu_backends
+    from paper_1711_01897_b200.discretization import (OperatorSpec, make_integration_context)
+    from paper_1711_01897_b200.errors import ConfigError
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix
+    v1, e1 = ico(1)
+    v2, e2 = ico(2)
+    spec, sp1, bt1 = setup(v1, e1, "p0", "laplace", "slp", 0.0)
+    _, sp2, bt2 = setup(v2, e2, "p0", "laplace", "slp", 0.0)
+    with pytest.raises(ConfigError, match="does not match"):
+        assemble_hmatrix(spec, sp1, sp1, bt2, AcaConfig())
+    other = OperatorSpec("helmholtz", "slp", 2.0)
+    wrong = make_gpu_backends(make_integration_context(other, sp1, sp1))
+    with pytest.raises(ConfigError, match="different operator spec"):
+        assemble_hmatrix(spec, sp1, sp1, bt1, AcaConfig(), wrong)
