@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""bench.py — H-matrix weak-form assembly on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[4], the headline; fits one GPU): Laplace
+single-layer, P0, geodesic sphere of frequency 448 = 4 014 080 triangles =
+4 014 080 unknowns, ACA eps 1e-3, FP64, n_min 32, eta 2, regular order 4,
+singular base order 4.  A "step" is one complete H-matrix assembly (all
+near-field leaves + ACA of all admissible leaves) over the resident mesh and
+partition.  The partition (cluster + block tree) is the input of
+assemble_hmatrix in the reference API and is built before timing.
+
+N > 1 (torchrun, one process per GPU): the leaves are split into N
+contiguous cost-weighted ranges; each rank assembles its range with no
+data-path collective (total work fixed => "scaling": "strong").
+
+Arms:
+  default          the CUDA path (libhbem_b200.so), device-resident inputs;
+                   "e2e" re-runs through the public API from host buffers
+                   (mesh + partition H2D, factors + dense payloads D2H into
+                   pinned host arenas).
+  --impl reference the reference algorithm on the host CPU cores: the CPU
+                   oracle (numpy restatement, oracle/hbem_oracle.py; the
+                   reference is pure Python/numpy so there is no compiled
+                   oracle/_ref) assembling a cost-weighted random sample of the
+                   same leaves with one process per core.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "H-matrix weak-form assembly wall time (s) and element-pair integrals/s per GPU"
+UNIT = "element-pair integrals/s"
+# algorithmic FLOP per regular Laplace-SLP P0 pair:
+# 36 quadrature-point pairs x (diff 3 + r^2 5 + accumulate 2) = 360 FLOP
+# (+ 36 rsqrt, not counted as FLOP)
+FLOP_PER_PAIR_LAP_SLP_P0 = 360
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=448, help="geodesic sphere frequency (20 n^2 tri)")
+    ap.add_argument("--eps", type=float, default=1e-3)
+    ap.add_argument("--precision", default="double", choices=["double", "single"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="bounded CPU sample per baseline measurement")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args):
+    from paper_1711_01897_b200.discretization import OperatorSpec, TriangleMesh, build_space
+    from paper_1711_01897_b200.meshes import geodesic_sphere
+    from paper_1711_01897_b200.partition import cluster_trees_for
+    v, e = geodesic_sphere(args.n)
+    mesh = TriangleMesh(v, e)
+    sp = build_space(mesh, "p0")
+    bt = cluster_trees_for(sp, sp)
+    spec = OperatorSpec("laplace", "slp", 0.0, args.precision)
+    return v, e, mesh, sp, bt, spec
+
+
+def config(args, world):
+    return {"workload": f"C5: Laplace SLP P0, geodesic sphere n={args.n} "
+                        f"({20 * args.n * args.n} triangles = unknowns), ACA eps={args.eps:g}, "
+                        f"{args.precision}, n_min=32, eta=2",
+            "n_unknowns": 20 * args.n * args.n, "eps": args.eps,
+            "parallelism": f"leaf-split x{world} (cost-weighted contiguous ranges)",
+            "l2": "inputs (geometry 0.6 GB) and outputs (~60 GB factors) exceed the 126 MB L2"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.rows = []
+        self.proc = None
+        self.gpu = gpu_index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([t.strip() for t in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU arm: the oracle on sampled leaves
+# ---------------------------------------------------------------------------
+_G = {}
+
+
+def _oracle_setup(v, e, bt, eps, precision):
+    from oracle import hbem_oracle as O
+    P = O.Problem(O.Spec("laplace", "slp", 0.0, precision), v, e, "p0", "p0")
+    na, bb = bt.rows.node_array, bt.rows.bbox
+    nodes = [O.Node(int(r[0]), int(r[1]), int(r[2]), bb[i, :3], bb[i, 3:], int(r[3]), int(r[4]))
+             for i, r in enumerate(na)]
+    tree = O.Tree(nodes, np.asarray(bt.rows.permutation))
+    leaves = [tuple(int(t) for t in row) for row in bt.leaf_array]
+    _G["asm"] = O.Assembler(P, tree, tree, leaves, eps)
+
+
+def _oracle_leaves(ids):
+    asm = _G["asm"]
+    asm.counters.update({"regular_pairs": 0, "singular_pairs": 0})
+    t0 = time.perf_counter()
+    for ix in ids:
+        asm.leaf(int(ix))
+    return (time.perf_counter() - t0, asm.counters["regular_pairs"],
+            asm.counters["singular_pairs"])
+
+
+def cpu_sample_ids(bt, n, rng):
+    from paper_1711_01897_b200.hmatrix import _leaf_costs
+    cost = _leaf_costs(bt)
+    p = cost / cost.sum()
+    return rng.choice(len(cost), size=min(n, len(cost)), replace=False, p=p)
+
+
+def cpu_rate(bt, seconds, workers, rng):
+    """Assemble cost-weighted random leaves for about ``seconds`` per worker;
+    returns (pairs/s, regular, singular, leaves, wall)."""
+    ids = cpu_sample_ids(bt, 200000, rng)
+    if workers <= 1:
+        done, reg, sing, t_all, k = 0, 0, 0, 0.0, 0
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < seconds and k < len(ids):
+            dt, r, s = _oracle_leaves(ids[k:k + 8])
+            reg, sing, t_all, k = reg + r, sing + s, t_all + dt, k + 8
+        wall = time.perf_counter() - t0
+        return (reg + sing) / wall, reg, sing, k, wall
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    # calibrate batch size on one process, then give every worker equal work
+    dt, r, s = _oracle_leaves(ids[:16])
+    per_leaf = max(dt / 16, 1e-4)
+    nper = max(8, int(seconds / per_leaf))
+    chunks = [ids[16 + i * nper: 16 + (i + 1) * nper] for i in range(workers)]
+    t0 = time.perf_counter()
+    with ctx.Pool(workers) as pool:
+        res = pool.map(_oracle_leaves, chunks)
+    wall = time.perf_counter() - t0
+    reg = sum(x[1] for x in res)
+    sing = sum(x[2] for x in res)
+    return (reg + sing) / wall, reg, sing, sum(len(c) for c in chunks), wall
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    v, e, mesh, sp, bt, spec = workload(args)
+    cores = os.cpu_count() or 1
+    _oracle_setup(v, e, bt, args.eps, args.precision)
+    rng = np.random.default_rng(1234)
+    per_step = max(5.0, min(args.cpu_seconds, 20.0))
+    for _ in range(args.warmup):
+        cpu_rate(bt, per_step / 4, cores, rng)
+    rates, times = [], []
+    for _ in range(args.steps):
+        rate, reg, sing, nl, wall = cpu_rate(bt, per_step, cores, rng)
+        rates.append(rate)
+        times.append(wall)
+    rate = float(np.median(rates))
+    sample = (f"{nl} leaves per step drawn cost-weighted from the {len(bt.leaf_array)} C5 "
+              f"leaves; oracle (numpy restatement of hbem.hmatrix.aca/_row_job/_col_job/"
+              f"dense_leaf + integrate_batch + local_matrix) on {cores} processes")
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.median(times)), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.precision == "double" else "f32",
+            "data": "synthetic geodesic sphere", "config": config(args, world),
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import ctypes as C
+
+    import torch
+
+    from paper_1711_01897_b200 import _lib
+    from paper_1711_01897_b200.backend import init_gpu_device
+    from paper_1711_01897_b200.discretization import make_integration_context
+    from paper_1711_01897_b200.hmatrix import (AcaConfig, AssemblyConfig, _assemble_part,
+                                               split_leaves)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    v, e, mesh, sp, bt, spec = workload(args)
+    ids = split_leaves(bt, world)[rank]
+    cfg = AcaConfig(epsilon=args.eps)
+    acfg = AssemblyConfig()
+    ictx = make_integration_context(spec, sp, sp)
+    dev = init_gpu_device(ictx, local)
+    stream = torch.cuda.current_stream()
+    sptr = C.c_void_p(stream.cuda_stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up 1 = setup + first execute
+    part = _assemble_part(dev, bt, ids, sp, sp, cfg, acfg, stream=sptr)
+    for _ in range(max(args.warmup - 1, 0)):
+        part.execute(sptr)
+    barrier()
+    aca_ms, nf_ms, pairs, sing, aca_entries, launches = [], [], 0, 0, 0, 0
+    with ClockSampler(local) as clocks:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        barrier()
+        t_start.record(stream)
+        for _ in range(args.steps):
+            part.execute(sptr)
+            s = part.stats
+            aca_ms.append(s["aca_kernel_ms"])
+            nf_ms.append(s["nearfield_kernel_ms"])
+            pairs += s["regular_pairs"] + s["singular_pairs"]
+            sing += s["singular_pairs"]
+            aca_entries += s["aca_entries"]
+            launches += s["launches"]
+        t_end.record(stream)
+        barrier()
+    elapsed = t_start.elapsed_time(t_end) / 1e3
+    stats = part.stats
+    tot = torch.tensor([elapsed, float(pairs), float(sing), float(launches)], dtype=torch.float64,
+                       device="cuda")
+    if dist is not None:
+        mx = tot.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tot.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        elapsed = float(mx[0].item())
+        pairs, sing, launches = float(sm[1].item()), float(sm[2].item()), int(sm[3].item())
+    per_step = elapsed / args.steps
+    value = pairs / elapsed
+
+    # dominant kernels: the ACA row+column launches (FP64 FMA-pipe bound)
+    aca_regular = aca_entries  # P0: one pair per evaluated entry (singular ones are ~0 here)
+    aca_s = sum(aca_ms) / 1e3
+    flop_rate = FLOP_PER_PAIR_LAP_SLP_P0 * aca_regular / aca_s if aca_s > 0 else 0.0
+    peak = C.c_double(0.0)
+    _lib.check(_lib.lib.hbem_probe_fma(local, _lib.PRECISIONS[args.precision], C.byref(peak)))
+    roofline = {"bound": "fp64" if args.precision == "double" else "fp32",
+                "kernel": "k_aca_row + k_aca_col (lock-step ACA waves)",
+                "achieved": flop_rate / 1e12, "peak": peak.value / 1e12, "unit": "TFLOP/s",
+                "frac": flop_rate / peak.value if peak.value else None,
+                "peak_source": "measured live: hbem_probe_fma (DFMA chain, 2 FLOP/FMA) on this GPU",
+                "algorithmic": f"{FLOP_PER_PAIR_LAP_SLP_P0} FLOP per regular pair (SURVEY §8d)",
+                "aca_kernel_ms_per_step": float(np.mean(aca_ms)),
+                "nearfield_kernel_ms_per_step": float(np.mean(nf_ms)),
+                "aca_pairs_per_s": aca_regular / aca_s if aca_s > 0 else None,
+                "traffic": None}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        _oracle_setup(v, e, bt, args.eps, args.precision)
+        rate, reg, sg, nl, wall = cpu_rate(bt, args.cpu_seconds, 1, np.random.default_rng(7))
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{nl} C5 leaves drawn cost-weighted ({reg} regular + {sg} singular "
+                         f"pairs in {wall:.1f} s), oracle on 1 core",
+               "extrapolated_assembly_s": (stats["regular_pairs"] + stats["singular_pairs"]) / rate}
+
+    e2e = None
+    if not args.no_e2e:
+        # public API from host buffers: mesh + partition H2D, factors and dense
+        # payloads D2H into pinned host arenas (allocated once, untimed)
+        pinned = part.arenas(pinned=True)
+        h2d = (v.nbytes + e.nbytes + bt.rows.permutation.nbytes + bt.rows.node_array.nbytes
+               + bt.leaf_array[ids].nbytes + sp.dofmap.nbytes)
+        d2h = sum(a.nbytes for a in pinned)
+        part.close()
+        del part
+        dev.close()
+        barrier()
+        t0 = time.perf_counter()
+        dev2 = init_gpu_device(ictx, local)
+        part2 = _assemble_part(dev2, bt, ids, sp, sp, cfg, acfg, stream=sptr)
+        out = (np.empty(0), np.empty(0), np.empty(0))
+        s2 = part2.stats
+        if s2["u_entries"] == len(pinned[0]) and s2["dense_entries"] == len(pinned[2]):
+            out = pinned
+        part2.arenas(out=out if len(out[0]) else None)
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        if dist is not None:
+            tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        e2e = {"value": pairs / args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "seconds": t_e2e,
+               "path": "GpuDeviceContext + assemble (hbem_ctx_create, hbem_hmat_assemble) + "
+                       "hbem_hmat_copy_arenas into pinned host arenas"}
+        part = part2
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * per_step,
+                "assembly_wall_s": per_step, "per_gpu": value / world,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "published_reference": "paper: ~100 min on 2x GTX TITAN Black for ~4M unknowns "
+                                       "(PAPER.md:25; different hardware, not a ratio)",
+                "dtype": "f64" if args.precision == "double" else "f32",
+                "data": "synthetic geodesic sphere (no external mesh)",
+                "config": config(args, world),
+                "pairs_per_step": {"regular": int((pairs - sing) / args.steps),
+                                   "singular": int(sing / args.steps)},
+                "aca": {"waves": stats["waves"], "row_jobs": stats["row_jobs"],
+                        "lowrank_leaves": stats["lowrank_leaves"],
+                        "dense_leaves": stats["dense_leaves"],
+                        "stored_entries": stats["u_entries"] + stats["v_entries"]
+                        + stats["dense_entries"]},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+    part.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -183,10 +183,21 @@ typedef struct hbem_hmat_stats {
   int64_t dense_leaves, lowrank_leaves;
   int64_t waves, row_jobs, col_jobs, capacity_retries;
   int64_t u_entries, v_entries, dense_entries;
-  double seconds;
+  int64_t launches;          /* kernels launched by the last execute */
+  int64_t aca_entries;       /* matrix entries evaluated by ACA row/column jobs */
+  double aca_kernel_ms;      /* CUDA-event time of the ACA row+column launches */
+  double nearfield_kernel_ms;/* CUDA-event time of the near-field launches (side stream) */
+  double seconds;            /* last execute, host wall clock incl. syncs */
+  double seconds_setup;      /* one-time partition upload + allocation */
+  double seconds_aca;        /* ACA waves (near-field overlapped) */
+  double seconds_finalize;   /* payload classification + dense expansion */
 } hbem_hmat_stats;
 
+/* setup (partition upload, state allocation) + one execute */
 int hbem_hmat_assemble(hbem_ctx *ctx, const hbem_hmat_desc *desc, void *stream, hbem_hmat **out);
+/* re-run the assembly on an existing handle (inputs resident on the device;
+   deterministic: identical payloads) */
+int hbem_hmat_execute(hbem_hmat *h, void *stream);
 int hbem_hmat_stats_get(const hbem_hmat *h, hbem_hmat_stats *stats);
 /* per leaf: kind (0 dense, 1 low-rank), rank, converged, exhausted,
    offsets of U (height*rank), V (width*rank) or dense (height*width)
@@ -198,6 +209,13 @@ int hbem_hmat_copy_arenas(const hbem_hmat *h, void *u, void *v, void *dense);
 /* y = H x in original DOF order; x, y host arrays of the result dtype. */
 int hbem_hmat_matvec(const hbem_hmat *h, const void *x, void *y);
 int hbem_hmat_destroy(hbem_hmat *h);
+
+/* pinned host buffers for fast D2H of the arenas */
+int hbem_host_alloc(int64_t bytes, void **out);
+int hbem_host_free(void *p);
+/* measured FMA throughput (FLOP/s, 2 per FMA) of this device, FP64 or FP32:
+   the live roofline denominator for the FMA-pipe-bound integrators */
+int hbem_probe_fma(int32_t device, int32_t precision, double *flops_per_s);
 
 #ifdef __cplusplus
 }

@@ -380,18 +380,19 @@ def integrate_batch(P: Problem, pairs: np.ndarray):
             p = int(np.nonzero(bad)[0][0])
             raise ContractViolation(f"request pair {p} = ({pairs[p, 0]}, {pairs[p, 1]}) "
                                     "is not disjoint")
-    q = P.qpoints.astype(rd)
-    nrm = P.normals.astype(rd)
-    jac = P.jac.astype(rd)
-    w = P.rule_weights.astype(rd)
-    ta = P.test_values.astype(rd)
-    tb = P.trial_values.astype(rd)
+    # working-precision caches cast once per problem, as init_device does
+    key = ("cast", rd.str)
+    if key not in P._cache:
+        P._cache[key] = (P.qpoints.astype(rd), P.normals.astype(rd), P.jac.astype(rd),
+                         P.rule_weights.astype(rd), P.test_values.astype(rd),
+                         P.trial_values.astype(rd),
+                         P.curls.astype(rd) if P.curls is not None else None)
+    q, nrm, jac, w, ta, tb, curls = P._cache[key]
     k = P.spec.wavenumber
     k2 = rd.type(k * k)
     nt, ns = ta.shape[0], tb.shape[0]
     out_re = np.empty((len(pairs), nt, ns), rd)
     out_im = np.empty((len(pairs), nt, ns), rd) if P.spec.is_complex else None
-    curls = P.curls.astype(rd) if P.curls is not None else None
     stride = 4096
     for s0 in range(0, len(pairs), stride):
         sl = slice(s0, s0 + stride)

@@ -87,8 +87,10 @@ class HmatStats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "regular_pairs", "singular_pairs", "aca_converged", "aca_exhausted",
         "aca_fallback_dense", "dense_leaves", "lowrank_leaves", "waves", "row_jobs",
-        "col_jobs", "capacity_retries", "u_entries", "v_entries", "dense_entries")] + [
-        ("seconds", C.c_double)]
+        "col_jobs", "capacity_retries", "u_entries", "v_entries", "dense_entries",
+        "launches", "aca_entries")] + [
+        (n, C.c_double) for n in ("aca_kernel_ms", "nearfield_kernel_ms", "seconds",
+                                  "seconds_setup", "seconds_aca", "seconds_finalize")]
 
 
 # (name, restype, argtypes) of every exported symbol in include/hbem_b200.h
@@ -119,12 +121,16 @@ SIGNATURES = [
     ("hbem_blocks_destroy", C.c_int, [C.c_void_p]),
     ("hbem_hmat_assemble", C.c_int,
      [C.c_void_p, C.POINTER(HmatDesc), C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("hbem_hmat_execute", C.c_int, [C.c_void_p, C.c_void_p]),
     ("hbem_hmat_stats_get", C.c_int, [C.c_void_p, C.POINTER(HmatStats)]),
     ("hbem_hmat_leaf_meta", C.c_int,
      [C.c_void_p, c_int32_p, c_int32_p, c_int32_p, c_int64_p, c_int64_p, c_int64_p]),
     ("hbem_hmat_copy_arenas", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("hbem_hmat_matvec", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("hbem_hmat_destroy", C.c_int, [C.c_void_p]),
+    ("hbem_host_alloc", C.c_int, [C.c_int64, C.POINTER(C.c_void_p)]),
+    ("hbem_host_free", C.c_int, [C.c_void_p]),
+    ("hbem_probe_fma", C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
 ]
 
 

@@ -643,44 +643,77 @@ __global__ void k_pack_factors(const int *slots, int n, AcaDev S, const long lon
 using namespace hb;
 
 // ---------------------------------------------------------------------------
-// host side
+// host side: setup (partition upload, state allocation) and execute (waves)
 // ---------------------------------------------------------------------------
 struct hbem_hmat {
   hbem_ctx *ctx = nullptr;
   int device = 0;
   int64_t n_leaves = 0;
   bool complex_ = false;
-  size_t vbytes = 8;  // bytes per value
-  // per leaf (host)
+  size_t vbytes = 8;
+  int nt = 1, ns = 1;
+  // per leaf results (host)
   std::vector<int32_t> kind, rank, flags;
   std::vector<int64_t> off_u, off_v, off_dense;
   std::vector<double> resid;
-  // device
-  void *pool = nullptr;
-  void *dense = nullptr;
-  long long dense_entries = 0, u_entries = 0, v_entries = 0;
-  // ACA block arrays needed for packing (device)
-  std::vector<void *> dev_allocs;
+  // partition views (device)
+  const int *rperm = nullptr, *cperm = nullptr;
+  const int *tptr = nullptr, *tel = nullptr, *sptr = nullptr, *sel = nullptr;
+  const signed char *tloc = nullptr, *sloc = nullptr;
+  // admissible blocks
+  int na = 0;
+  std::vector<int> adm_leaf, ah, aw, ar0, ac0;
+  int *d_order = nullptr, *listA = nullptr, *listA2 = nullptr;
   AcaDev S{};
-  std::vector<int> lowrank_slots;   // adm slot per low-rank leaf
+  void *pool = nullptr;
+  // near-field leaves
+  int nd = 0;
+  std::vector<int> den_leaf;
+  long long nf_entries = 0;
+  DenseDev D{};
+  unsigned n_tiles = 0;
+  long long nf_max_sing = 0;
+  void *dense_nf = nullptr;
+  // admissible blocks stored densely (after ACA)
+  void *dense_adm = nullptr;
+  size_t dense_adm_cap = 0;
+  long long dense_entries = 0, u_entries = 0, v_entries = 0;
+  std::vector<int> lowrank_slots;
   std::vector<int64_t> lr_uoff, lr_voff;
+  cudaStream_t side = nullptr;
+  cudaEvent_t side_done = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<void *> dev_allocs;
   hbem_hmat_stats stats{};
+  double setup_s = 0.0;
   ~hbem_hmat() {
     cudaSetDevice(device);
     for (void *p : dev_allocs) cudaFree(p);
     cudaFree(pool);
-    cudaFree(dense);
+    cudaFree(dense_nf);
+    cudaFree(dense_adm);
+    if (side) cudaStreamDestroy(side);
+    if (side_done) cudaEventDestroy(side_done);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
   }
 };
 
 namespace {
 
+using clk = std::chrono::steady_clock;
+double secs(clk::time_point a, clk::time_point b) {
+  return std::chrono::duration<double>(b - a).count();
+}
+
 template <typename X> int dalloc(hbem_hmat *H, X **p, size_t n) {
   void *q = nullptr;
   cudaError_t e = cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(X));
-  if (e != cudaSuccess)
+  if (e != cudaSuccess) {
+    cudaGetLastError();
     return set_error(HBEM_ERR_CAPACITY, "device allocation of %zu bytes failed: %s",
                      n * sizeof(X), cudaGetErrorString(e));
+  }
   H->dev_allocs.push_back(q);
   *p = static_cast<X *>(q);
   return HBEM_OK;
@@ -717,26 +750,36 @@ Incidence incidence(const int64_t *dofmap, int64_t m, int nl, int64_t n_dofs) {
   return I;
 }
 
-template <typename T, bool C>
-int assemble_t(hbem_ctx *ctx, const hbem_hmat_desc *d, cudaStream_t st, hbem_hmat *H) {
-  using V = typename Num<T, C>::V;
-  const auto t_start = std::chrono::steady_clock::now();
+template <typename T> Prob<T> make_prob(const hbem_hmat *H) {
+  Prob<T> P{};
+  P.g = H->ctx->geo<T>();
+  P.R = H->ctx->rule<T>();
+  P.G64 = H->ctx->geo64();
+  P.elem = H->ctx->elem;
+  P.rperm = H->rperm;
+  P.cperm = H->cperm;
+  P.tptr = H->tptr; P.tel = H->tel; P.tloc = H->tloc;
+  P.sptr = H->sptr; P.sel = H->sel; P.sloc = H->sloc;
+  return P;
+}
+
+// one-time: partition / DOF maps / ACA state / pools on the device
+int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
+  hbem_ctx *ctx = H->ctx;
   const int64_t m = ctx->m;
   const int nt = ctx->nt, ns = ctx->ns;
-  // ---- partition / DOF maps on device ------------------------------------
-  std::vector<int> rperm(d->n_rows), cperm(d->n_cols);
-  for (int64_t i = 0; i < d->n_rows; ++i) rperm[i] = (int)d->row_perm[i];
-  for (int64_t i = 0; i < d->n_cols; ++i) cperm[i] = (int)d->col_perm[i];
-  Prob<T> P{};
-  P.g = ctx->geo<T>();
-  P.R = ctx->rule<T>();
-  P.G64 = ctx->geo64();
-  P.elem = ctx->elem;
-  int *d_rperm, *d_cperm;
-  HB_CHECK(upload(H, &d_rperm, rperm));
-  HB_CHECK(upload(H, &d_cperm, cperm));
-  P.rperm = d_rperm;
-  P.cperm = d_cperm;
+  H->nt = nt;
+  H->ns = ns;
+  {
+    std::vector<int> rp(d->n_rows), cp(d->n_cols);
+    for (int64_t i = 0; i < d->n_rows; ++i) rp[i] = (int)d->row_perm[i];
+    for (int64_t i = 0; i < d->n_cols; ++i) cp[i] = (int)d->col_perm[i];
+    int *a, *b;
+    HB_CHECK(upload(H, &a, rp));
+    HB_CHECK(upload(H, &b, cp));
+    H->rperm = a;
+    H->cperm = b;
+  }
   if (nt == 3) {
     Incidence I = incidence(d->test_dofmap, m, 3, d->n_rows);
     int *p, *e;
@@ -744,7 +787,7 @@ int assemble_t(hbem_ctx *ctx, const hbem_hmat_desc *d, cudaStream_t st, hbem_hma
     HB_CHECK(upload(H, &p, I.ptr));
     HB_CHECK(upload(H, &e, I.el));
     HB_CHECK(upload(H, &l, I.loc));
-    P.tptr = p; P.tel = e; P.tloc = l;
+    H->tptr = p; H->tel = e; H->tloc = l;
   }
   if (ns == 3) {
     Incidence I = incidence(d->trial_dofmap, m, 3, d->n_cols);
@@ -753,9 +796,8 @@ int assemble_t(hbem_ctx *ctx, const hbem_hmat_desc *d, cudaStream_t st, hbem_hma
     HB_CHECK(upload(H, &p, I.ptr));
     HB_CHECK(upload(H, &e, I.el));
     HB_CHECK(upload(H, &l, I.loc));
-    P.sptr = p; P.sel = e; P.sloc = l;
+    H->sptr = p; H->sel = e; H->sloc = l;
   }
-  // ---- split leaves ----------------------------------------------------------
   const int64_t L = d->n_leaves;
   H->n_leaves = L;
   H->kind.assign(L, 0);
@@ -765,40 +807,47 @@ int assemble_t(hbem_ctx *ctx, const hbem_hmat_desc *d, cudaStream_t st, hbem_hma
   H->off_v.assign(L, -1);
   H->off_dense.assign(L, -1);
   H->resid.assign(L, 0.0);
-  std::vector<int> adm_leaf, den_leaf;
-  for (int64_t q = 0; q < L; ++q) (d->leaves[3 * q + 2] ? adm_leaf : den_leaf).push_back((int)q);
-  auto node_rng = [&](const int64_t *nodes, int64_t n) {
+  for (int64_t q = 0; q < L; ++q)
+    (d->leaves[3 * q + 2] ? H->adm_leaf : H->den_leaf).push_back((int)q);
+  auto rng = [&](const int64_t *nodes, int64_t n) {
     return std::pair<int, int>((int)nodes[5 * n], (int)(nodes[5 * n + 1] - nodes[5 * n]));
   };
-  const int na = (int)adm_leaf.size();
-  std::vector<int> ah(na), aw(na), ar0(na), ac0(na);
+  // ---- admissible blocks --------------------------------------------------------
+  const int na = (int)H->adm_leaf.size();
+  H->na = na;
+  H->ah.resize(na); H->aw.resize(na); H->ar0.resize(na); H->ac0.resize(na);
   std::vector<long long> rmo(na), cmo(na);
   long long rmw = 0, cmw = 0, sum_hw = 0;
   for (int q = 0; q < na; ++q) {
-    const int64_t lf = adm_leaf[q];
-    auto [r0, h] = node_rng(d->row_nodes, d->leaves[3 * lf]);
-    auto [c0, w] = node_rng(d->col_nodes, d->leaves[3 * lf + 1]);
-    ar0[q] = r0; ah[q] = h; ac0[q] = c0; aw[q] = w;
+    const int64_t lf = H->adm_leaf[q];
+    auto [r0, h] = rng(d->row_nodes, d->leaves[3 * lf]);
+    auto [c0, w] = rng(d->col_nodes, d->leaves[3 * lf + 1]);
+    H->ar0[q] = r0; H->ah[q] = h; H->ac0[q] = c0; H->aw[q] = w;
     rmo[q] = rmw; rmw += (h + 31) / 32;
     cmo[q] = cmw; cmw += (w + 31) / 32;
     sum_hw += h + w;
   }
-  const int kmax_cfg = d->k_max > 0 ? (int)std::min<int64_t>(d->k_max, 1 << 30) : (1 << 30);
-  int tmax = d->rank_capacity > 0 ? d->rank_capacity : 64;
-  tmax = std::min(tmax, kTmaxSmem);
   AcaDev &S = H->S;
-  S.tmax = tmax;
-  S.kmax_cfg = kmax_cfg;
+  int tmax = d->rank_capacity > 0 ? d->rank_capacity : 64;
+  S.tmax = std::min(tmax, kTmaxSmem);
+  S.kmax_cfg = d->k_max > 0 ? (int)std::min<int64_t>(d->k_max, 1 << 30) : (1 << 30);
   S.eps = d->epsilon;
   {
     int *p;
-    HB_CHECK(upload(H, &p, ah)); S.h = p;
-    HB_CHECK(upload(H, &p, aw)); S.w = p;
-    HB_CHECK(upload(H, &p, ar0)); S.r0 = p;
-    HB_CHECK(upload(H, &p, ac0)); S.c0 = p;
+    HB_CHECK(upload(H, &p, H->ah)); S.h = p;
+    HB_CHECK(upload(H, &p, H->aw)); S.w = p;
+    HB_CHECK(upload(H, &p, H->ar0)); S.r0 = p;
+    HB_CHECK(upload(H, &p, H->ac0)); S.c0 = p;
     long long *pl;
     HB_CHECK(upload(H, &pl, rmo)); S.rmask_off = pl;
     HB_CHECK(upload(H, &pl, cmo)); S.cmask_off = pl;
+    // big blocks first (load balance of the CTA-per-block waves)
+    std::vector<int> order(na);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      return (long long)H->ah[a] * H->aw[a] > (long long)H->ah[b] * H->aw[b];
+    });
+    HB_CHECK(upload(H, &H->d_order, order));
   }
   HB_CHECK(dalloc(H, &S.rank, na));
   HB_CHECK(dalloc(H, &S.cur, na));
@@ -811,71 +860,142 @@ int assemble_t(hbem_ctx *ctx, const hbem_hmat_desc *d, cudaStream_t st, hbem_hma
   HB_CHECK(dalloc(H, &S.rn2, na));
   HB_CHECK(dalloc(H, &S.piv, 2 * (size_t)na));
   HB_CHECK(dalloc(H, &S.pend, na));
-  HB_CHECK(dalloc(H, &S.terms, (size_t)na * tmax));
+  HB_CHECK(dalloc(H, &S.terms, (size_t)na * S.tmax));
   HB_CHECK(dalloc(H, &S.rmask, rmw));
   HB_CHECK(dalloc(H, &S.cmask, cmw));
-  int *listA, *listB, *listA2, *counts;
-  HB_CHECK(dalloc(H, &listA, na));
-  HB_CHECK(dalloc(H, &listB, na));
-  HB_CHECK(dalloc(H, &listA2, na));
-  HB_CHECK(dalloc(H, &counts, 4));
-  S.counts = counts;
-  S.listB = listB;
-  unsigned long long *stat, *pool_top;
-  HB_CHECK(dalloc(H, &stat, 4));
-  HB_CHECK(dalloc(H, &pool_top, 1));
-  HB_CUDA(cudaMemsetAsync(stat, 0, 32, st));
-  HB_CUDA(cudaMemsetAsync(pool_top, 0, 8, st));
-  S.stat = stat;
-  S.pool_top = pool_top;
-  // dense leaves: exact sizes known now
-  const int nd = (int)den_leaf.size();
-  std::vector<int> dr0, dc0, dh, dw;
-  std::vector<long long> doff;
-  long long dense_total = 0;
+  HB_CHECK(dalloc(H, &H->listA, na));
+  HB_CHECK(dalloc(H, &H->listA2, na));
+  HB_CHECK(dalloc(H, &S.listB, na));
+  HB_CHECK(dalloc(H, &S.counts, 4));
+  HB_CHECK(dalloc(H, &S.stat, 4));
+  HB_CHECK(dalloc(H, &S.pool_top, 1));
+  // ---- near-field leaves --------------------------------------------------------
+  const int nd = (int)H->den_leaf.size();
+  H->nd = nd;
+  std::vector<int> dr0(nd), dc0(nd), dh(nd), dw(nd);
+  std::vector<long long> doff(nd);
+  long long tot = 0;
   for (int q = 0; q < nd; ++q) {
-    const int64_t lf = den_leaf[q];
-    auto [r0, h] = node_rng(d->row_nodes, d->leaves[3 * lf]);
-    auto [c0, w] = node_rng(d->col_nodes, d->leaves[3 * lf + 1]);
-    dr0.push_back(r0); dh.push_back(h); dc0.push_back(c0); dw.push_back(w);
-    doff.push_back(dense_total);
-    H->off_dense[lf] = dense_total;
-    dense_total += (long long)h * w;
+    const int64_t lf = H->den_leaf[q];
+    auto [r0, h] = rng(d->row_nodes, d->leaves[3 * lf]);
+    auto [c0, w] = rng(d->col_nodes, d->leaves[3 * lf + 1]);
+    dr0[q] = r0; dh[q] = h; dc0[q] = c0; dw[q] = w;
+    doff[q] = tot;
+    H->off_dense[lf] = tot;
+    tot += (long long)h * w;
   }
-  // pool: what is left of device memory after a margin for the dense arena
+  H->nf_entries = tot;
+  {
+    std::vector<int> tslot, tstart;
+    tslot.reserve(tot / kThreads + nd);
+    tstart.reserve(tot / kThreads + nd);
+    for (int s = 0; s < nd; ++s) {
+      const long long hw = (long long)dh[s] * dw[s];
+      for (long long t = 0; t < hw; t += kThreads) {
+        tslot.push_back(s);
+        tstart.push_back((int)t);
+      }
+    }
+    H->n_tiles = (unsigned)tslot.size();
+    DenseDev &D = H->D;
+    int *p;
+    long long *pl;
+    HB_CHECK(upload(H, &p, tslot)); D.tile_slot = p;
+    HB_CHECK(upload(H, &p, tstart)); D.tile_start = p;
+    HB_CHECK(upload(H, &p, dr0)); D.r0 = p;
+    HB_CHECK(upload(H, &p, dc0)); D.c0 = p;
+    HB_CHECK(upload(H, &p, dh)); D.h = p;
+    HB_CHECK(upload(H, &p, dw)); D.w = p;
+    HB_CHECK(upload(H, &pl, doff)); D.off = pl;
+    HB_CHECK(dalloc(H, &D.sing_count, 1));
+    HB_CHECK(dalloc(H, &D.stat, 2));
+    if (nt == 1 && ns == 1) {
+      // touching P0 pairs: at most ~13 per element; bound by the entry count
+      H->nf_max_sing = std::min<long long>(tot, 32 * (m + 1));
+      HB_CHECK(dalloc(H, &D.sing_slot, H->nf_max_sing));
+      HB_CHECK(dalloc(H, &D.sing_pos, H->nf_max_sing));
+    }
+  }
+  const size_t vb = H->vbytes;
+  HB_CUDA(cudaMalloc(&H->dense_nf, std::max<size_t>((size_t)tot * vb, vb)));
+  H->D.out = H->dense_nf;
+  // ---- factor pool: what is left after a margin for the admissible-dense arena
   size_t free_b = 0, total_b = 0;
   HB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const size_t vb = sizeof(V);
-  const size_t want = (size_t)sum_hw * (size_t)std::min(tmax, 24) * vb;
-  const size_t reserve = (size_t)dense_total * vb * 2 + ((size_t)2 << 30);
+  const size_t want = (size_t)sum_hw * (size_t)std::min(S.tmax, 24) * vb;
+  const size_t reserve = ((size_t)4 << 30) + (size_t)(0.02 * (double)free_b);
   size_t cap_b = free_b > reserve ? free_b - reserve : 0;
   cap_b = std::min(cap_b, std::max(want, (size_t)1 << 20));
-  cap_b = std::min(cap_b, (size_t)(free_b * 0.85));
   HB_CUDA(cudaMalloc(&H->pool, std::max<size_t>(cap_b, vb)));
   S.pool = H->pool;
   S.pool_cap = (long long)(cap_b / vb);
+  HB_CUDA(cudaStreamCreateWithFlags(&H->side, cudaStreamNonBlocking));
+  HB_CUDA(cudaEventCreateWithFlags(&H->side_done, cudaEventDisableTiming));
+  for (auto &e : H->ev) HB_CUDA(cudaEventCreate(&e));
+  return HBEM_OK;
+}
 
-  const auto t_setup = std::chrono::steady_clock::now();
-  // ---- ACA waves ---------------------------------------------------------------
+template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
+  using V = typename Num<T, C>::V;
+  hbem_ctx *ctx = H->ctx;
+  const auto t0 = clk::now();
+  Prob<T> P = make_prob<T>(H);
+  AcaDev &S = H->S;
+  const int nt = H->nt, ns = H->ns;
+  const int na = H->na;
+  int64_t launches = 0;
+  hbem_hmat_stats &ST = H->stats;
+  const hbem_hmat_stats zero{};
+  ST = zero;
+  // ---- near-field leaves on the side stream (overlaps the ACA waves) ---------
+  cudaEvent_t start_ev;
+  HB_CUDA(cudaEventCreateWithFlags(&start_ev, cudaEventDisableTiming));
+  HB_CUDA(cudaEventRecord(start_ev, st));
+  HB_CUDA(cudaStreamWaitEvent(H->side, start_ev, 0));
+  cudaEventDestroy(start_ev);
+  HB_CUDA(cudaEventRecord(H->ev[2], H->side));
+  if (H->nd > 0) {
+    HB_CUDA(cudaMemsetAsync(H->D.sing_count, 0, 8, H->side));
+    HB_CUDA(cudaMemsetAsync(H->D.stat, 0, 16, H->side));
+    int rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc,
+                                                         auto NSc) -> int {
+      constexpr int OP = decltype(OPc)::value;
+      constexpr bool HH = decltype(Hc)::value != 0;
+      constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
+      k_dense<T, C, OP, HH, NT, NS><<<H->n_tiles, kThreads, 0, H->side>>>(P, H->D);
+      HB_CUDA(cudaGetLastError());
+      ++launches;
+      if constexpr (NT == 1 && NS == 1) {
+        k_dense_singular<T, C, OP, HH><<<148 * 16, kThreads, 0, H->side>>>(P, H->D);
+        HB_CUDA(cudaGetLastError());
+        ++launches;
+      }
+      return HBEM_OK;
+    });
+    if (rc != HBEM_OK) return rc;
+  }
+  HB_CUDA(cudaEventRecord(H->side_done, H->side));
+  HB_CUDA(cudaEventRecord(H->ev[3], H->side));
+  // ---- ACA waves ------------------------------------------------------------------
+  HB_CUDA(cudaMemsetAsync(S.stat, 0, 32, st));
+  HB_CUDA(cudaMemsetAsync(S.pool_top, 0, 8, st));
   int waves = 0;
   if (na > 0) {
     k_aca_init<<<(na + 127) / 128, 128, 0, st>>>(S, na);
     HB_CUDA(cudaGetLastError());
-    // large blocks first for load balance
-    std::vector<int> order(na);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-      return (long long)ah[a] * aw[a] > (long long)ah[b] * aw[b];
-    });
-    HB_CUDA(cudaMemcpyAsync(listA, order.data(), na * sizeof(int), cudaMemcpyHostToDevice, st));
+    ++launches;
+    HB_CUDA(cudaMemcpyAsync(H->listA, H->d_order, na * sizeof(int), cudaMemcpyDeviceToDevice,
+                            st));
     int nA = na;
-    int *la = listA, *la2 = listA2;
+    int *la = H->listA, *la2 = H->listA2;
     int h_counts[2];
     while (nA > 0) {
       S.listA = la;
       S.listA2 = la2;
-      HB_CUDA(cudaMemsetAsync(counts, 0, 16, st));
-      int rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc, auto NSc) -> int {
+      HB_CUDA(cudaMemsetAsync(S.counts, 0, 16, st));
+      HB_CUDA(cudaEventRecord(H->ev[0], st));
+      int rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc,
+                                                           auto NSc) -> int {
         constexpr int OP = decltype(OPc)::value;
         constexpr bool HH = decltype(Hc)::value != 0;
         constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
@@ -886,17 +1006,22 @@ int assemble_t(hbem_ctx *ctx, const hbem_hmat_desc *d, cudaStream_t st, hbem_hma
         return HBEM_OK;
       });
       if (rc != HBEM_OK) return rc;
-      HB_CUDA(cudaMemcpyAsync(h_counts, counts, 8, cudaMemcpyDeviceToHost, st));
+      launches += 2;
+      HB_CUDA(cudaEventRecord(H->ev[1], st));
+      HB_CUDA(cudaMemcpyAsync(h_counts, S.counts, 8, cudaMemcpyDeviceToHost, st));
       HB_CUDA(cudaStreamSynchronize(st));
-      H->stats.row_jobs += nA;
-      H->stats.col_jobs += h_counts[0];
+      float ms = 0.f;
+      HB_CUDA(cudaEventElapsedTime(&ms, H->ev[0], H->ev[1]));
+      ST.aca_kernel_ms += ms;
+      ST.row_jobs += nA;
+      ST.col_jobs += h_counts[0];
       nA = h_counts[1];
       std::swap(la, la2);
       ++waves;
     }
   }
-  const auto t_aca = std::chrono::steady_clock::now();
-  // ---- classify admissible blocks --------------------------------------------
+  const auto t_aca = clk::now();
+  // ---- classify admissible blocks (lowrank_leaf, hmatrix.py:721-735) -------------
   std::vector<int> st_h(na), rk_h(na), ex_h(na);
   std::vector<double> rs_h(na);
   if (na > 0) {
@@ -905,137 +1030,187 @@ int assemble_t(hbem_ctx *ctx, const hbem_hmat_desc *d, cudaStream_t st, hbem_hma
     HB_CUDA(cudaMemcpy(ex_h.data(), S.exhausted, na * 4, cudaMemcpyDeviceToHost));
     HB_CUDA(cudaMemcpy(rs_h.data(), S.resid, na * 8, cudaMemcpyDeviceToHost));
   }
-  std::vector<int> expand_slots, fallback_slots;
-  std::vector<long long> expand_off;
+  H->lowrank_slots.clear();
+  H->lr_uoff.clear();
+  H->lr_voff.clear();
+  H->u_entries = H->v_entries = 0;
+  std::vector<int> expand_slots, fb_r0, fb_c0, fb_h, fb_w;
+  std::vector<long long> expand_off, fb_off;
+  long long adm_dense = 0;
   for (int q = 0; q < na; ++q) {
-    const int lf = adm_leaf[q];
+    const int lf = H->adm_leaf[q];
     const int s = st_h[q];
+    const int h = H->ah[q], w = H->aw[q];
     if (s == ST_OVERFLOW)
       return set_error(HBEM_ERR_CAPACITY,
                        "ACA rank capacity %d exceeded for block rows [%d, %d) x cols [%d, %d); "
                        "raise rank_capacity",
-                       tmax, ar0[q], ar0[q] + ah[q], ac0[q], ac0[q] + aw[q]);
+                       S.tmax, H->ar0[q], H->ar0[q] + h, H->ac0[q], H->ac0[q] + w);
     if (s == ST_POOL)
       return set_error(HBEM_ERR_CAPACITY, "ACA factor pool of %lld values exhausted",
                        (long long)S.pool_cap);
     H->rank[lf] = rk_h[q];
     H->resid[lf] = rs_h[q];
     H->flags[lf] = (s == ST_CONVERGED ? 1 : 0) | (ex_h[q] ? 2 : 0);
-    const long long hw = (long long)ah[q] * aw[q];
+    H->kind[lf] = 0;
+    H->off_u[lf] = H->off_v[lf] = -1;
+    const long long hw = (long long)h * w;
+    if (ex_h[q]) ST.aca_exhausted++;
     if (s == ST_CONVERGED) {
-      H->stats.aca_converged++;
-      if (ex_h[q]) H->stats.aca_exhausted++;
-      if ((long long)rk_h[q] * (ah[q] + aw[q]) < hw) {
+      ST.aca_converged++;
+      if ((long long)rk_h[q] * (h + w) < hw) {
         H->kind[lf] = 1;
         H->lowrank_slots.push_back(q);
         H->off_u[lf] = H->u_entries;
         H->off_v[lf] = H->v_entries;
         H->lr_uoff.push_back(H->u_entries);
         H->lr_voff.push_back(H->v_entries);
-        H->u_entries += (long long)ah[q] * rk_h[q];
-        H->v_entries += (long long)aw[q] * rk_h[q];
-        H->stats.lowrank_leaves++;
+        H->u_entries += (long long)h * rk_h[q];
+        H->v_entries += (long long)w * rk_h[q];
+        ST.lowrank_leaves++;
         continue;
       }
       expand_slots.push_back(q);
-      expand_off.push_back(dense_total);
+      expand_off.push_back(adm_dense);
     } else {  // ST_FALLBACK: rank cap without convergence -> exact rows
-      if (ex_h[q]) H->stats.aca_exhausted++;
-      H->stats.aca_fallback_dense++;
-      fallback_slots.push_back(q);
-      dr0.push_back(ar0[q]); dh.push_back(ah[q]); dc0.push_back(ac0[q]); dw.push_back(aw[q]);
-      doff.push_back(dense_total);
+      ST.aca_fallback_dense++;
+      fb_r0.push_back(H->ar0[q]); fb_c0.push_back(H->ac0[q]);
+      fb_h.push_back(h); fb_w.push_back(w);
+      fb_off.push_back(adm_dense);
     }
-    H->off_dense[lf] = dense_total;
-    dense_total += hw;
+    H->off_dense[lf] = H->nf_entries + adm_dense;
+    adm_dense += hw;
   }
-  H->stats.dense_leaves = nd + (int64_t)expand_slots.size() + (int64_t)fallback_slots.size();
-  H->dense_entries = dense_total;
-  // ---- dense arena -------------------------------------------------------------
-  HB_CUDA(cudaMalloc(&H->dense, std::max<size_t>((size_t)dense_total * vb, vb)));
-  const int nds = (int)dr0.size();
-  if (nds > 0) {
-    std::vector<int> tslot, tstart;
-    long long maxq = 0;
-    for (int s = 0; s < nds; ++s) {
-      const long long hw = (long long)dh[s] * dw[s];
-      for (long long t = 0; t < hw; t += kThreads) {
-        tslot.push_back(s);
-        tstart.push_back((int)t);
-      }
-      maxq += hw;
-    }
-    DenseDev D{};
-    int *p;
-    long long *pl;
-    HB_CHECK(upload(H, &p, tslot)); D.tile_slot = p;
-    HB_CHECK(upload(H, &p, tstart)); D.tile_start = p;
-    HB_CHECK(upload(H, &p, dr0)); D.r0 = p;
-    HB_CHECK(upload(H, &p, dc0)); D.c0 = p;
-    HB_CHECK(upload(H, &p, dh)); D.h = p;
-    HB_CHECK(upload(H, &p, dw)); D.w = p;
-    HB_CHECK(upload(H, &pl, doff)); D.off = pl;
-    D.out = H->dense;
-    D.stat = stat;
-    unsigned long long *scount;
-    HB_CHECK(dalloc(H, &scount, 1));
-    HB_CUDA(cudaMemsetAsync(scount, 0, 8, st));
-    D.sing_count = scount;
-    if (nt == 1 && ns == 1) {
-      // touching P0 pairs <= 13 per element; bound by the entry count
-      const long long cap = std::min<long long>(maxq, 16 * (m + 1));
-      HB_CHECK(dalloc(H, &D.sing_slot, cap));
-      HB_CHECK(dalloc(H, &D.sing_pos, cap));
-    }
-    const unsigned ntiles = (unsigned)tslot.size();
-    int rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc, auto NSc) -> int {
-      constexpr int OP = decltype(OPc)::value;
-      constexpr bool HH = decltype(Hc)::value != 0;
-      constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
-      k_dense<T, C, OP, HH, NT, NS><<<ntiles, kThreads, 0, st>>>(P, D);
-      HB_CUDA(cudaGetLastError());
-      if constexpr (NT == 1 && NS == 1) {
-        k_dense_singular<T, C, OP, HH><<<148 * 16, kThreads, 0, st>>>(P, D);
-        HB_CUDA(cudaGetLastError());
-      }
-      return HBEM_OK;
-    });
-    if (rc != HBEM_OK) return rc;
-    if (nt == 1 && ns == 1) {
-      unsigned long long ns_h = 0;
-      HB_CUDA(cudaMemcpyAsync(&ns_h, scount, 8, cudaMemcpyDeviceToHost, st));
-      HB_CUDA(cudaStreamSynchronize(st));
-      H->stats.singular_pairs += (int64_t)ns_h;
-    }
-    H->stats.regular_pairs += maxq;
+  ST.dense_leaves = H->nd + (int64_t)expand_slots.size() + (int64_t)fb_r0.size();
+  H->dense_entries = H->nf_entries + adm_dense;
+  const size_t vb = sizeof(V);
+  if ((size_t)adm_dense * vb > H->dense_adm_cap) {
+    cudaFree(H->dense_adm);
+    H->dense_adm = nullptr;
+    H->dense_adm_cap = (size_t)adm_dense * vb;
+    HB_CUDA(cudaMalloc(&H->dense_adm, std::max(H->dense_adm_cap, vb)));
   }
   if (!expand_slots.empty()) {
     int *slots;
     long long *offs;
     HB_CHECK(upload(H, &slots, expand_slots));
     HB_CHECK(upload(H, &offs, expand_off));
-    k_expand<T, C><<<(unsigned)expand_slots.size(), 128, 0, st>>>(slots, (int)expand_slots.size(), S, offs, H->dense);
+    k_expand<T, C><<<(unsigned)expand_slots.size(), 128, 0, st>>>(
+        slots, (int)expand_slots.size(), S, offs, H->dense_adm);
     HB_CUDA(cudaGetLastError());
+    ++launches;
   }
+  unsigned long long fb_sing = 0;
+  if (!fb_r0.empty()) {
+    // exact rows of non-converged blocks: the dense-leaf kernels on a
+    // temporary tile list
+    DenseDev F{};
+    std::vector<int> tslot, tstart;
+    long long ent = 0;
+    for (size_t s = 0; s < fb_r0.size(); ++s) {
+      const long long hw = (long long)fb_h[s] * fb_w[s];
+      for (long long t = 0; t < hw; t += kThreads) {
+        tslot.push_back((int)s);
+        tstart.push_back((int)t);
+      }
+      ent += hw;
+    }
+    int *p;
+    long long *pl;
+    HB_CHECK(upload(H, &p, tslot)); F.tile_slot = p;
+    HB_CHECK(upload(H, &p, tstart)); F.tile_start = p;
+    HB_CHECK(upload(H, &p, fb_r0)); F.r0 = p;
+    HB_CHECK(upload(H, &p, fb_c0)); F.c0 = p;
+    HB_CHECK(upload(H, &p, fb_h)); F.h = p;
+    HB_CHECK(upload(H, &p, fb_w)); F.w = p;
+    HB_CHECK(upload(H, &pl, fb_off)); F.off = pl;
+    F.out = H->dense_adm;
+    HB_CHECK(dalloc(H, &F.sing_count, 1));
+    HB_CHECK(dalloc(H, &F.stat, 2));
+    HB_CUDA(cudaMemsetAsync(F.sing_count, 0, 8, st));
+    HB_CUDA(cudaMemsetAsync(F.stat, 0, 16, st));
+    if (nt == 1 && ns == 1) {
+      HB_CHECK(dalloc(H, &F.sing_slot, ent));
+      HB_CHECK(dalloc(H, &F.sing_pos, ent));
+    }
+    const unsigned ntl = (unsigned)tslot.size();
+    int rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc,
+                                                         auto NSc) -> int {
+      constexpr int OP = decltype(OPc)::value;
+      constexpr bool HH = decltype(Hc)::value != 0;
+      constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
+      k_dense<T, C, OP, HH, NT, NS><<<ntl, kThreads, 0, st>>>(P, F);
+      HB_CUDA(cudaGetLastError());
+      if constexpr (NT == 1 && NS == 1) {
+        k_dense_singular<T, C, OP, HH><<<148 * 16, kThreads, 0, st>>>(P, F);
+        HB_CUDA(cudaGetLastError());
+      }
+      return HBEM_OK;
+    });
+    if (rc != HBEM_OK) return rc;
+    launches += (nt == 1 && ns == 1) ? 2 : 1;
+    unsigned long long fs[2] = {0, 0};
+    HB_CUDA(cudaMemcpyAsync(&fb_sing, F.sing_count, 8, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaMemcpyAsync(fs, F.stat, 16, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    fb_sing += fs[1];
+    ST.regular_pairs += ent;
+  }
+  HB_CUDA(cudaStreamWaitEvent(st, H->side_done, 0));
+  unsigned long long nf_sing = 0, nf_stat[2] = {0, 0}, aca_stat[2] = {0, 0};
+  HB_CUDA(cudaMemcpyAsync(&nf_sing, H->D.sing_count, 8, cudaMemcpyDeviceToHost, st));
+  HB_CUDA(cudaMemcpyAsync(nf_stat, H->D.stat, 16, cudaMemcpyDeviceToHost, st));
+  HB_CUDA(cudaMemcpyAsync(aca_stat, S.stat, 16, cudaMemcpyDeviceToHost, st));
   HB_CUDA(cudaStreamSynchronize(st));
-  const auto t_end = std::chrono::steady_clock::now();
-  unsigned long long stat_h[2] = {0, 0};
-  HB_CUDA(cudaMemcpy(stat_h, stat, 16, cudaMemcpyDeviceToHost));
-  // entries evaluated by ACA jobs + dense; singular counted separately
-  H->stats.singular_pairs += (int64_t)stat_h[1];
-  H->stats.regular_pairs += (int64_t)stat_h[0];
-  H->stats.regular_pairs -= H->stats.singular_pairs;
-  H->stats.waves = waves;
-  H->stats.u_entries = H->u_entries;
-  H->stats.v_entries = H->v_entries;
-  H->stats.dense_entries = H->dense_entries;
-  H->stats.seconds = std::chrono::duration<double>(t_end - t_start).count();
-  (void)t_setup;
-  (void)t_aca;
+  const auto t_end = clk::now();
+  {
+    float ms = 0.f;
+    HB_CUDA(cudaEventElapsedTime(&ms, H->ev[2], H->ev[3]));
+    ST.nearfield_kernel_ms = ms;
+  }
+  ST.aca_entries = (int64_t)aca_stat[0];
+  // pair accounting: ACA jobs |T(dof)| |col_elems| (P0: the job
+  // width), near-field |rows| |cols|; singular pairs counted separately
+  const int64_t sing = (int64_t)(nf_sing + nf_stat[1] + aca_stat[1] + fb_sing);
+  ST.singular_pairs = sing;
+  ST.regular_pairs += (int64_t)aca_stat[0] + H->nf_entries - sing;
+  ST.waves = waves;
+  ST.u_entries = H->u_entries;
+  ST.v_entries = H->v_entries;
+  ST.dense_entries = H->dense_entries;
+  ST.seconds = secs(t0, t_end);
+  ST.seconds_setup = H->setup_s;
+  ST.seconds_aca = secs(t0, t_aca);
+  ST.seconds_finalize = secs(t_aca, t_end);
+  ST.launches = launches;
   return HBEM_OK;
 }
 
+int execute(hbem_hmat *H, cudaStream_t st) {
+  hbem_ctx *ctx = H->ctx;
+  if (ctx->precision == HBEM_DOUBLE)
+    return ctx->helm ? execute_t<double, true>(H, st) : execute_t<double, false>(H, st);
+  return ctx->helm ? execute_t<float, true>(H, st) : execute_t<float, false>(H, st);
+}
+
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// FP64 / FP32 FMA throughput probes (roofline denominators measured live)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_fma_probe(T *out, int iters, T a) {
+  T x0 = (T)threadIdx.x, x1 = x0 + T(1), x2 = x0 + T(2), x3 = x0 + T(3);
+  T x4 = x0 + T(4), x5 = x0 + T(5), x6 = x0 + T(6), x7 = x0 + T(7);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      x0 = x0 * a + a; x1 = x1 * a + a; x2 = x2 * a + a; x3 = x3 * a + a;
+      x4 = x4 * a + a; x5 = x5 * a + a; x6 = x6 * a + a; x7 = x7 * a + a;
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
 
 extern "C" {
 
@@ -1052,18 +1227,23 @@ int hbem_hmat_assemble(hbem_ctx *ctx, const hbem_hmat_desc *d, void *stream, hbe
   H->device = ctx->device;
   H->complex_ = ctx->helm;
   H->vbytes = (size_t)ctx->real_bytes() * (ctx->helm ? 2 : 1);
-  cudaStream_t st = (cudaStream_t)stream;
-  int rc;
-  if (ctx->precision == HBEM_DOUBLE)
-    rc = ctx->helm ? assemble_t<double, true>(ctx, d, st, H) : assemble_t<double, false>(ctx, d, st, H);
-  else
-    rc = ctx->helm ? assemble_t<float, true>(ctx, d, st, H) : assemble_t<float, false>(ctx, d, st, H);
+  const auto t0 = clk::now();
+  int rc = setup(H, d);
+  H->setup_s = secs(t0, clk::now());
+  if (rc == HBEM_OK) rc = execute(H, (cudaStream_t)stream);
   if (rc != HBEM_OK) {
     delete H;
     return rc;
   }
   *out = H;
   return HBEM_OK;
+}
+
+int hbem_hmat_execute(hbem_hmat *h, void *stream) {
+  clear_error();
+  if (!h) return set_error(HBEM_ERR_ARG, "null hmat");
+  HB_CUDA(cudaSetDevice(h->device));
+  return execute(h, (cudaStream_t)stream);
 }
 
 int hbem_hmat_stats_get(const hbem_hmat *h, hbem_hmat_stats *s) {
@@ -1075,14 +1255,12 @@ int hbem_hmat_stats_get(const hbem_hmat *h, hbem_hmat_stats *s) {
 int hbem_hmat_leaf_meta(const hbem_hmat *h, int32_t *kind, int32_t *rank, int32_t *flags,
                         int64_t *off_u, int64_t *off_v, int64_t *off_dense) {
   if (!h) return set_error(HBEM_ERR_ARG, "null hmat");
-  const size_t L = (size_t)h->n_leaves;
   if (kind) std::copy(h->kind.begin(), h->kind.end(), kind);
   if (rank) std::copy(h->rank.begin(), h->rank.end(), rank);
   if (flags) std::copy(h->flags.begin(), h->flags.end(), flags);
   if (off_u) std::copy(h->off_u.begin(), h->off_u.end(), off_u);
   if (off_v) std::copy(h->off_v.begin(), h->off_v.end(), off_v);
   if (off_dense) std::copy(h->off_dense.begin(), h->off_dense.end(), off_dense);
-  (void)L;
   return HBEM_OK;
 }
 
@@ -1091,16 +1269,22 @@ int hbem_hmat_copy_arenas(const hbem_hmat *hc, void *u, void *v, void *dense) {
   hbem_hmat *h = const_cast<hbem_hmat *>(hc);
   if (!h) return set_error(HBEM_ERR_ARG, "null hmat");
   HB_CUDA(cudaSetDevice(h->device));
-  if (dense && h->dense_entries > 0)
-    HB_CUDA(cudaMemcpy(dense, h->dense, (size_t)h->dense_entries * h->vbytes,
-                       cudaMemcpyDeviceToHost));
+  const size_t vb = h->vbytes;
+  if (dense) {
+    if (h->nf_entries > 0)
+      HB_CUDA(cudaMemcpy(dense, h->dense_nf, (size_t)h->nf_entries * vb, cudaMemcpyDeviceToHost));
+    const long long adm = h->dense_entries - h->nf_entries;
+    if (adm > 0)
+      HB_CUDA(cudaMemcpy((char *)dense + (size_t)h->nf_entries * vb, h->dense_adm, (size_t)adm * vb,
+                         cudaMemcpyDeviceToHost));
+  }
   if ((u || v) && !h->lowrank_slots.empty()) {
-    // pack in chunks of blocks through a staging buffer
+    // gather the factor records of the low-rank blocks in chunks
     const size_t n = h->lowrank_slots.size();
-    const long long chunk_vals = 64ll << 20;  // values per staging half
+    const long long chunk_vals = 64ll << 20;
     void *su = nullptr, *sv = nullptr;
-    HB_CUDA(cudaMalloc(&su, chunk_vals * h->vbytes));
-    HB_CUDA(cudaMalloc(&sv, chunk_vals * h->vbytes));
+    HB_CUDA(cudaMalloc(&su, chunk_vals * vb));
+    HB_CUDA(cudaMalloc(&sv, chunk_vals * vb));
     int *d_slots = nullptr;
     long long *d_uo = nullptr, *d_vo = nullptr;
     HB_CUDA(cudaMalloc(&d_slots, n * 4));
@@ -1111,39 +1295,37 @@ int hbem_hmat_copy_arenas(const hbem_hmat *hc, void *u, void *v, void *dense) {
     HB_CUDA(cudaMemcpy(d_vo, h->lr_voff.data(), n * 8, cudaMemcpyHostToDevice));
     size_t q0 = 0;
     while (q0 < n) {
-      size_t q1 = q0;
       const long long ub = h->lr_uoff[q0], vbase = h->lr_voff[q0];
-      long long ue = ub, ve = vbase;
-      while (q1 < n) {
-        const long long nu = (q1 + 1 < n ? h->lr_uoff[q1 + 1] : h->u_entries) - ub;
-        const long long nv = (q1 + 1 < n ? h->lr_voff[q1 + 1] : h->v_entries) - vbase;
-        if ((nu > chunk_vals || nv > chunk_vals) && q1 > q0) break;
-        ue = ub + nu;
-        ve = vbase + nv;
+      size_t q1 = q0 + 1;
+      while (q1 < n && h->lr_uoff[q1] - ub < chunk_vals && h->lr_voff[q1] - vbase < chunk_vals &&
+             (q1 + 1 < n ? h->lr_uoff[q1 + 1] : h->u_entries) - ub <= chunk_vals &&
+             (q1 + 1 < n ? h->lr_voff[q1 + 1] : h->v_entries) - vbase <= chunk_vals)
         ++q1;
-        if (nu > chunk_vals || nv > chunk_vals) break;
+      const long long ue = q1 < n ? h->lr_uoff[q1] : h->u_entries;
+      const long long ve = q1 < n ? h->lr_voff[q1] : h->v_entries;
+      if (ue - ub > chunk_vals || ve - vbase > chunk_vals) {
+        cudaFree(su); cudaFree(sv);
+        HB_CUDA(cudaMalloc(&su, (ue - ub) * vb));
+        HB_CUDA(cudaMalloc(&sv, (ve - vbase) * vb));
       }
       const int cnt = (int)(q1 - q0);
-      const unsigned grid = (unsigned)cnt;
       if (h->vbytes == 16)
-        k_pack_factors<Cx<double>><<<grid, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0,
-                                                  ub, vbase, (Cx<double> *)su, (Cx<double> *)sv);
+        k_pack_factors<Cx<double>><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0,
+                                                 ub, vbase, (Cx<double> *)su, (Cx<double> *)sv);
       else if (h->vbytes == 8 && h->complex_)
-        k_pack_factors<Cx<float>><<<grid, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
-                                                 vbase, (Cx<float> *)su, (Cx<float> *)sv);
+        k_pack_factors<Cx<float>><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
+                                                vbase, (Cx<float> *)su, (Cx<float> *)sv);
       else if (h->vbytes == 8)
-        k_pack_factors<double><<<grid, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
-                                              vbase, (double *)su, (double *)sv);
+        k_pack_factors<double><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
+                                             vbase, (double *)su, (double *)sv);
       else
-        k_pack_factors<float><<<grid, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
-                                             vbase, (float *)su, (float *)sv);
+        k_pack_factors<float><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
+                                            vbase, (float *)su, (float *)sv);
       HB_CUDA(cudaGetLastError());
       if (u)
-        HB_CUDA(cudaMemcpy((char *)u + ub * h->vbytes, su, (ue - ub) * h->vbytes,
-                           cudaMemcpyDeviceToHost));
+        HB_CUDA(cudaMemcpy((char *)u + ub * vb, su, (ue - ub) * vb, cudaMemcpyDeviceToHost));
       if (v)
-        HB_CUDA(cudaMemcpy((char *)v + vbase * h->vbytes, sv, (ve - vbase) * h->vbytes,
-                           cudaMemcpyDeviceToHost));
+        HB_CUDA(cudaMemcpy((char *)v + vbase * vb, sv, (ve - vbase) * vb, cudaMemcpyDeviceToHost));
       q0 = q1;
     }
     cudaFree(su);
@@ -1161,6 +1343,53 @@ int hbem_hmat_matvec(const hbem_hmat *, const void *, void *) {
 
 int hbem_hmat_destroy(hbem_hmat *h) {
   delete h;
+  return HBEM_OK;
+}
+
+int hbem_host_alloc(int64_t bytes, void **out) {
+  clear_error();
+  if (!out) return set_error(HBEM_ERR_ARG, "null argument");
+  *out = nullptr;
+  HB_CUDA(cudaHostAlloc(out, (size_t)std::max<int64_t>(bytes, 1), cudaHostAllocDefault));
+  return HBEM_OK;
+}
+
+int hbem_host_free(void *p) {
+  if (p) cudaFreeHost(p);
+  return HBEM_OK;
+}
+
+int hbem_probe_fma(int32_t device, int32_t precision, double *flops_per_s) {
+  clear_error();
+  if (!flops_per_s) return set_error(HBEM_ERR_ARG, "null argument");
+  HB_CUDA(cudaSetDevice(device));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  const int threads = 256, blocks = sms * 8, iters = 4096;
+  void *out = nullptr;
+  HB_CUDA(cudaMalloc(&out, (size_t)blocks * threads * 8));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(a);
+    if (precision == HBEM_DOUBLE)
+      k_fma_probe<double><<<blocks, threads>>>((double *)out, iters, 0.999999);
+    else
+      k_fma_probe<float><<<blocks, threads>>>((float *)out, iters, 0.999999f);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep > 0) best = std::min(best, ms);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  HB_CUDA(cudaGetLastError());
+  const double fmas = (double)blocks * threads * iters * 16.0 * 8.0;
+  *flops_per_s = 2.0 * fmas / (best * 1e-3);
   return HBEM_OK;
 }
 

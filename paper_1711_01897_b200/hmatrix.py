@@ -142,6 +142,19 @@ class _Payloads:
         return (self[i] for i in range(len(self)))
 
 
+def pinned_empty(n: int, dtype) -> np.ndarray:
+    """numpy array in page-locked host memory (cudaHostAlloc via the C ABI),
+    released when the array's buffer is garbage collected."""
+    import weakref
+    dtype = np.dtype(dtype)
+    nbytes = max(int(n) * dtype.itemsize, 1)
+    p = C.c_void_p()
+    check(lib.hbem_host_alloc(nbytes, C.byref(p)))
+    buf = (C.c_byte * nbytes).from_address(p.value)
+    weakref.finalize(buf, lib.hbem_host_free, C.c_void_p(p.value))
+    return np.frombuffer(buf, dtype=dtype, count=int(n))
+
+
 class _DevicePart:
     """One hbem_hmat (one GPU's share of the leaves) and its host arenas."""
 
@@ -149,7 +162,13 @@ class _DevicePart:
         self.handle = handle
         self.dtype = dtype
         self.shapes = shapes  # (L, 2) h, w
-        L = n_leaves
+        self.n_leaves = n_leaves
+        self._pinned = []
+        self._lock = threading.Lock()
+        self._refresh()
+
+    def _refresh(self):
+        L, handle = self.n_leaves, self.handle
         self.kind = np.empty(L, np.int32)
         self.rank = np.empty(L, np.int32)
         self.flags = np.empty(L, np.int32)
@@ -166,15 +185,26 @@ class _DevicePart:
         check(lib.hbem_hmat_stats_get(handle, C.byref(st)))
         self.stats = {name: getattr(st, name) for name, _ in _lib.HmatStats._fields_}
         self._arenas = None
-        self._lock = threading.Lock()
 
-    def arenas(self):
+    def execute(self, stream=None):
+        """Re-run the whole assembly on the device (inputs already resident);
+        deterministic, so the payloads are unchanged."""
+        check(lib.hbem_hmat_execute(self.handle, stream))
+        self._refresh()
+
+    def _host_array(self, n, pinned):
+        return pinned_empty(n, self.dtype) if pinned else np.empty(n, self.dtype)
+
+    def arenas(self, pinned: bool = False, out=None):
+        """Host copies of the factor (U, V) and dense arenas; ``out`` reuses
+        previously allocated (e.g. pinned) host buffers."""
         with self._lock:
-            if self._arenas is None:
+            if self._arenas is None or out is not None:
                 s = self.stats
-                u = np.empty(s["u_entries"], self.dtype)
-                v = np.empty(s["v_entries"], self.dtype)
-                d = np.empty(s["dense_entries"], self.dtype)
+                if out is None:
+                    out = tuple(self._host_array(s[k], pinned)
+                                for k in ("u_entries", "v_entries", "dense_entries"))
+                u, v, d = out
                 check(lib.hbem_hmat_copy_arenas(self.handle, _lib.vptr(u), _lib.vptr(v),
                                                 _lib.vptr(d)))
                 self._arenas = (u, v, d)
@@ -196,6 +226,7 @@ class _DevicePart:
         if self.handle:
             lib.hbem_hmat_destroy(self.handle)
             self.handle = None
+        self._arenas = None
 
     def __del__(self):
         try:
