@@ -30,6 +30,8 @@
 #include <numeric>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "hbem_internal.h"
 
 namespace hb {
@@ -157,35 +159,46 @@ __device__ __forceinline__ typename Num<T, C>::V entry(const Prob<T> &P, int di,
 // ---------------------------------------------------------------------------
 enum : int { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_FALLBACK = 2, ST_OVERFLOW = 3, ST_POOL = 4 };
 
+constexpr int kThreads = 128;
+constexpr int kWarps = kThreads / 32;
+constexpr int kE = 2;                  // entries per integration thread
+constexpr int kChunk = kThreads * kE;  // entries per integration CTA
+
+// Each accepted rank-1 term is one pool record [u (h) | v (w)]; v is stored
+// scaled (v = row / pivot, hmatrix.py:339) once the update is accepted.
 struct AcaDev {
   const int *h, *w, *r0, *c0;
   int *rank, *cur, *pcol, *small, *status, *exhausted;
-  double *norm2, *resid, *rn2, *piv;  // piv: 2 doubles (re, im)
+  double *norm2, *resid, *rn2, *piv;  // piv: pivot of the pending row (re, im)
   long long *pend, *terms;
   int tmax;
   unsigned *rmask, *cmask;
   const long long *rmask_off, *cmask_off;
   void *pool;
-  long long pool_cap;
-  unsigned long long *pool_top;
+  long long pool_cap, pool_base;
   int kmax_cfg;
   double eps;
+  // wave lists: A (row phase), C (column phase), A2 (next wave)
   const int *listA;
-  int *listB, *listA2, *counts;  // counts[0] = |B|, counts[1] = |A2|
-  unsigned long long *stat;      // [0] entries, [1] singular pairs
+  const longlong2 *needA, *scanA;  // (chunks, pool values) per position, inclusive scan
+  int *listC;
+  long long *needC;                // column chunks per position
+  const long long *scanC;
+  int *listA2;
+  longlong2 *needA2;
+  int *counts;                     // [0] |C|, [1] |A2|, [2] singular queue length
+  int2 *squeue;                    // (position, entry index) of touching P0 pairs
+  int squeue_cap;
+  unsigned long long *stat;        // [0] entries evaluated, [1] singular pairs
+  struct Job *jobs;                // per position of the current phase
+  int *cmap;                       // chunk -> position
+  void *coef;                      // per position: tmax residual coefficients
 };
-
-constexpr int kThreads = 128;
-constexpr int kWarps = kThreads / 32;
-constexpr int kTmaxSmem = 96;
 
 __device__ __forceinline__ bool better(double a, int ia, double b, int ib) {
   return a > b || (a == b && ia < ib);
 }
-
-// block-wide argmax (first index on ties) and sum; result valid in thread 0
-__device__ __forceinline__ void block_reduce(double &best, int &bidx, double &sum, double *s_v,
-                                             int *s_i, double *s_s) {
+__device__ __forceinline__ void warp_argmax_sum(double &best, int &bidx, double &sum) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const double ob = __shfl_xor_sync(0xffffffffu, best, o);
@@ -193,21 +206,11 @@ __device__ __forceinline__ void block_reduce(double &best, int &bidx, double &su
     if (better(ob, oi, best, bidx)) { best = ob; bidx = oi; }
     sum += __shfl_xor_sync(0xffffffffu, sum, o);
   }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) { s_v[warp] = best; s_i[warp] = bidx; s_s[warp] = sum; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 1; k < kWarps; ++k) {
-      if (better(s_v[k], s_i[k], best, bidx)) { best = s_v[k]; bidx = s_i[k]; }
-      sum += s_s[k];
-    }
-  }
 }
-
 __device__ __forceinline__ bool bit(const unsigned *m, int i) { return (m[i >> 5] >> (i & 31)) & 1u; }
 __device__ __forceinline__ void set_bit(unsigned *m, int i) { atomicOr(m + (i >> 5), 1u << (i & 31)); }
 
-// lowest row without its bit set (padding bits are preset), or -1
+// lowest index without its bit set (padding bits preset), or -1
 __device__ int first_clear(const unsigned *m, int n) {
   const int nw = (n + 31) >> 5;
   for (int k = 0; k < nw; ++k) {
@@ -220,294 +223,381 @@ __device__ int first_clear(const unsigned *m, int n) {
   return -1;
 }
 
+__device__ __forceinline__ int upper_pos(const long long *scan, int n, long long x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (scan[mid] > x) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+__device__ __forceinline__ int upper_pos2(const longlong2 *scan, int n, long long x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (scan[mid].x > x) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ long long row_slot(const AcaDev &S, int pos, int b) {
+  const long long pe = S.pend[b];
+  return pe >= 0 ? pe : S.pool_base + S.scanA[pos].y - S.needA[pos].y;
+}
+
+__host__ __device__ __forceinline__ long long chunks_of(int n) { return (n + kChunk - 1) / kChunk; }
+
+// regular P0 pair value with the element data of one side already loaded
+template <typename T, bool C, int OP, bool HELM>
+__device__ __forceinline__ typename Num<T, C>::V p0_value(const Prob<T> &P, const T (&x)[18],
+                                                          const T (&na)[4], int f) {
+  T y[18], nb[4], re[1][1], im[1][1];
+  load_q<T>(P.g.q, f, y);
+  load_nj<T>(P.g.nj, f, nb);
+  regular_pair<T, OP, HELM, 1, 1>(P.R, x, y, na, nb, nullptr, nullptr, re, im);
+  return Num<T, C>::mk(re[0][0], im[0][0]);
+}
+template <typename T, bool C, int OP, bool HELM>
+__device__ __forceinline__ typename Num<T, C>::V p0_value_col(const Prob<T> &P, int e,
+                                                              const T (&y)[18],
+                                                              const T (&nb)[4]) {
+  T x[18], na[4], re[1][1], im[1][1];
+  load_q<T>(P.g.q, e, x);
+  load_nj<T>(P.g.nj, e, na);
+  regular_pair<T, OP, HELM, 1, 1>(P.R, x, y, na, nb, nullptr, nullptr, re, im);
+  return Num<T, C>::mk(re[0][0], im[0][0]);
+}
+
 // ---------------------------------------------------------------------------
-// K3a: ACA row phase.  One CTA per active block.
+// Per-wave job tables.  After the chunk scan, one thread per job packs what
+// the integration threads need (block shape, fixed element, pending pool
+// slot, first chunk) into one record, fills the chunk -> job map and gathers
+// the residual coefficients (row phase: u_l[i]; column phase: v_l[j]), so an
+// integration thread reaches its geometry through two loads.
 // ---------------------------------------------------------------------------
-template <typename T, bool C, int OP, bool HELM, int NT, int NS>
-__global__ void __launch_bounds__(kThreads) k_aca_row(Prob<T> P, AcaDev S) {
+struct Job {
+  int b, h, w, k;
+  int fix;        // row phase: row i; column phase: column j
+  int r0, c0;
+  int elem;       // DOF of the fixed side (test DOF of row i / trial DOF of column j)
+  long long pe;   // pending pool slot of this block
+  long long cbase;
+};
+
+template <typename V>
+__global__ void k_jobs(AcaDev S, const int *list, int n, int col_phase, const int *rperm,
+                       const int *cperm) {
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= n) return;
+  const int b = list[pos];
+  Job J;
+  J.b = b;
+  J.h = S.h[b];
+  J.w = S.w[b];
+  J.k = S.rank[b];
+  J.r0 = S.r0[b];
+  J.c0 = S.c0[b];
+  long long c1;
+  if (!col_phase) {
+    J.fix = S.cur[b];
+    J.pe = row_slot(S, pos, b);
+    J.elem = rperm[J.r0 + J.fix];
+    J.cbase = pos ? S.scanA[pos - 1].x : 0;
+    c1 = S.scanA[pos].x;
+  } else {
+    J.fix = S.pcol[b];
+    J.pe = S.pend[b];
+    J.elem = cperm[J.c0 + J.fix];
+    J.cbase = pos ? S.scanC[pos - 1] : 0;
+    c1 = S.scanC[pos];
+  }
+  for (long long ch = J.cbase; ch < c1; ++ch) S.cmap[ch] = pos;
+  const V *pool = static_cast<const V *>(S.pool);
+  V *coef = static_cast<V *>(S.coef) + (long long)pos * S.tmax;
+  const long long *tl = S.terms + (long long)b * S.tmax;
+  for (int l = 0; l < J.k; ++l)
+    coef[l] = col_phase ? pool[tl[l] + J.h + J.fix] : pool[tl[l] + J.fix];
+  S.jobs[pos] = J;
+}
+
+// ---------------------------------------------------------------------------
+// K3a/K3b: ACA row / column integration.  One CTA = one chunk of kChunk
+// entries of one job; each thread evaluates kE entries (integral, residual
+// update with the gathered coefficients, store).  No barriers.
+//   row:    val(c) = A(i, c) - sum_l u_l[i] v_l[c]   (hmatrix.py:323-327)
+//   column: val(r) = A(r, j) - sum_l v_l[j] u_l[r]   (hmatrix.py:340-342)
+// ---------------------------------------------------------------------------
+template <typename T, bool C, int OP, bool HELM, int NT, int NS, bool COL>
+__global__ void __launch_bounds__(kThreads) k_int(Prob<T> P, AcaDev S) {
   using N = Num<T, C>;
   using V = typename N::V;
-  __shared__ V s_u[kTmaxSmem];
-  __shared__ long long s_term[kTmaxSmem];
-  __shared__ double s_v[kWarps], s_s[kWarps];
-  __shared__ int s_i[kWarps];
-  __shared__ int s_stop;
-  __shared__ long long s_pend;
-  const int b = S.listA[blockIdx.x];
-  const int h = S.h[b], w = S.w[b];
-  const int k = S.rank[b];
-  const int i = S.cur[b];
+  const int pos = S.cmap[blockIdx.x];
+  const Job J = S.jobs[pos];
+  const int base = (int)(blockIdx.x - J.cbase) * kChunk;
+  const int n = COL ? J.h : J.w;
+  if (base + (int)threadIdx.x >= n) return;
   V *pool = static_cast<V *>(S.pool);
-  if (threadIdx.x == 0) {
-    int stop = 0;
-    const int kmax_b = min(S.kmax_cfg, min(h, w));
-    if (k >= kmax_b) {                   // rank cap without convergence
-      S.status[b] = ST_FALLBACK;
-      stop = 1;
-    } else if (k >= S.tmax) {            // term table exhausted: retry bigger
-      S.status[b] = ST_OVERFLOW;
-      stop = 1;
-    } else if (i < 0) {                  // rows exhausted (hmatrix.py:319-322)
-      S.status[b] = ST_CONVERGED;
-      S.exhausted[b] = 1;
-      stop = 1;
-    } else {
-      long long pe = S.pend[b];
-      if (pe < 0) {
-        const unsigned long long o = atomicAdd(S.pool_top, (unsigned long long)(h + w));
-        if ((long long)o + h + w > S.pool_cap) {
-          S.status[b] = ST_POOL;
-          stop = 1;
-        } else {
-          pe = (long long)o;
-          S.pend[b] = pe;
-        }
-      }
-      s_pend = pe;
-      atomicAdd(S.stat, (unsigned long long)w);
-    }
-    s_stop = stop;
-  }
-  if (i >= 0)
-    for (int l = threadIdx.x; l < k && l < S.tmax; l += kThreads) {
-      const long long t = S.terms[(long long)b * S.tmax + l];
-      s_term[l] = t;
-      s_u[l] = pool[t + i];
-    }
-  __syncthreads();
-  if (s_stop) return;
-  const long long pe = s_pend;
-  V *row = pool + pe + h;
-  const unsigned *cm = S.cmask + S.cmask_off[b];
-  const int r0 = S.r0[b], c0 = S.c0[b];
-  const int di = P.rperm[r0 + i];
-  double best = -1.0, ss = 0.0;
-  int bidx = 0x7fffffff;
-
+  const V *coef = static_cast<const V *>(S.coef) + (long long)pos * S.tmax;
+  const long long *tl = S.terms + (long long)J.b * S.tmax;
+  const int vofs = COL ? 0 : J.h;  // residual factor read at [t + vofs + idx]
+  V *dst = pool + J.pe + vofs;
+  T x[18], nx[4];
   if constexpr (NT == 1 && NS == 1) {
-    // P0: the test element is fixed for the whole row
-    T x[18], na[4];
-    load_q<T>(P.g.q, di, x);
-    load_nj<T>(P.g.nj, di, na);
-    const int4 ea = P.elem[di];
-    for (int c = threadIdx.x; c < w; c += kThreads) {
-      const int f = P.cperm[c0 + c];
-      V val;
-      if (touching(ea, P.elem[f])) {
-        val = entry<T, C, OP, HELM, 1, 1>(P, di, f, S.stat + 1);
-      } else {
-        T y[18], nb[4], re[1][1], im[1][1];
-        load_q<T>(P.g.q, f, y);
-        load_nj<T>(P.g.nj, f, nb);
-        regular_pair<T, OP, HELM, 1, 1>(P.R, x, y, na, nb, nullptr, nullptr, re, im);
-        val = N::mk(re[0][0], im[0][0]);
-      }
-      for (int l = 0; l < k; ++l) val = N::fms(val, s_u[l], pool[s_term[l] + h + c]);
-      row[c] = val;
-      const double a = N::abs(val);
-      ss += N::nrm(val);
-      if (!bit(cm, c) && a > best) { best = a; bidx = c; }
-    }
-  } else {
-    for (int c = threadIdx.x; c < w; c += kThreads) {
-      const int dj = P.cperm[c0 + c];
-      V val = entry<T, C, OP, HELM, NT, NS>(P, di, dj, S.stat + 1);
-      for (int l = 0; l < k; ++l) val = N::fms(val, s_u[l], pool[s_term[l] + h + c]);
-      row[c] = val;
-      const double a = N::abs(val);
-      ss += N::nrm(val);
-      if (!bit(cm, c) && a > best) { best = a; bidx = c; }
-    }
+    load_q<T>(P.g.q, J.elem, x);
+    load_nj<T>(P.g.nj, J.elem, nx);
   }
-  block_reduce(best, bidx, ss, s_v, s_i, s_s);
-  if (threadIdx.x == 0) {
-    if (best <= 0.0) {
-      // residual row vanished: retire it to Z, restart from the lowest
-      // unused row (hmatrix.py:334-338); no column job this wave
-      unsigned *rm = S.rmask + S.rmask_off[b];
-      set_bit(rm, i);
-      __threadfence_block();
-      S.cur[b] = first_clear(rm, h);
-      S.listA2[atomicAdd(S.counts + 1, 1)] = b;
-    } else {
-      const V pv = row[bidx];
-      S.pcol[b] = bidx;
-      if constexpr (C) {
-        S.piv[2 * b] = pv.re;
-        S.piv[2 * b + 1] = pv.im;
-      } else {
-        S.piv[2 * b] = pv;
-        S.piv[2 * b + 1] = 0.0;
+  const int4 efix = P.elem[J.elem];
+#pragma unroll 1
+  for (int e = 0; e < kE; ++e) {
+    const int idx = base + e * kThreads + threadIdx.x;
+    if (idx >= n) break;
+    const int dof = COL ? P.rperm[J.r0 + idx] : P.cperm[J.c0 + idx];
+    V val;
+    if constexpr (NT == 1 && NS == 1) {
+      if (touching(efix, P.elem[dof])) {
+        const int q = atomicAdd(S.counts + 2, 1);
+        if (q < S.squeue_cap) S.squeue[q] = make_int2(pos, idx);
+        continue;
       }
-      S.rn2[b] = ss;
-      S.listB[atomicAdd(S.counts, 1)] = b;
+      if (COL) val = p0_value_col<T, C, OP, HELM>(P, dof, x, nx);
+      else val = p0_value<T, C, OP, HELM>(P, x, nx, dof);
+    } else {
+      val = COL ? entry<T, C, OP, HELM, NT, NS>(P, dof, J.elem, S.stat + 1)
+                : entry<T, C, OP, HELM, NT, NS>(P, J.elem, dof, S.stat + 1);
+    }
+    const int ro = COL ? 0 : J.h;  // where the other factor of term l lives
+    for (int l = 0; l < J.k; ++l) val = N::fms(val, coef[l], pool[tl[l] + ro + idx]);
+    dst[idx] = val;
+  }
+}
+
+// touching P0 pairs queued by the integration kernels: warp per pair
+// (Sauter-Schwab in float64, kernels.py:249-290), then the same residual.
+template <typename T, bool C, int OP, bool HELM>
+__global__ void __launch_bounds__(kThreads) k_int_singular(Prob<T> P, AcaDev S, int col_phase) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int n = min(S.counts[2], S.squeue_cap);
+  V *pool = static_cast<V *>(S.pool);
+  for (int q = warp; q < n; q += nw) {
+    const int2 it = S.squeue[q];
+    const Job J = S.jobs[it.x];
+    const int idx = it.y;
+    const int row = col_phase ? idx : J.fix, col = col_phase ? J.fix : idx;
+    const int e = P.rperm[J.r0 + row], f = P.cperm[J.c0 + col];
+    double re[1][1], im[1][1];
+    singular_local<OP, HELM, 1, 1, 32>(P.G64, e, f, re, im);
+    if (lane == 0) {
+      V val = N::mk((T)re[0][0], (T)im[0][0]);
+      const V *coef = static_cast<const V *>(S.coef) + (long long)it.x * S.tmax;
+      const long long *tl = S.terms + (long long)J.b * S.tmax;
+      const int ro = col_phase ? 0 : J.h;
+      for (int l = 0; l < J.k; ++l) val = N::fms(val, coef[l], pool[tl[l] + ro + idx]);
+      pool[J.pe + (col_phase ? 0 : J.h) + idx] = val;
+      atomicAdd(S.stat + 1, 1ull);
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// K3b: ACA column phase + stopping test + Frobenius update + next pivot.
+// K3c: row finalize, warp per block: column pivot (argmax |row| over unused
+// columns, first index on ties), vanishing-row test, schedule the column job.
 // ---------------------------------------------------------------------------
-template <typename T, bool C, int OP, bool HELM, int NT, int NS>
-__global__ void __launch_bounds__(kThreads) k_aca_col(Prob<T> P, AcaDev S) {
+template <typename T, bool C>
+__global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int nA) {
   using N = Num<T, C>;
   using V = typename N::V;
-  __shared__ V s_v[kTmaxSmem];
-  __shared__ long long s_term[kTmaxSmem];
-  __shared__ double s_bv[kWarps], s_ss[kWarps];
-  __shared__ int s_bi[kWarps];
-  __shared__ double s_dot[kTmaxSmem][kWarps][4];
-  __shared__ int s_accept;
-  if ((int)blockIdx.x >= S.counts[0]) return;
-  const int b = S.listB[blockIdx.x];
-  const int h = S.h[b], w = S.w[b];
-  const int k = S.rank[b];
-  const int i = S.cur[b];
-  const int j = S.pcol[b];
-  const long long pe = S.pend[b];
-  V *pool = static_cast<V *>(S.pool);
-  for (int l = threadIdx.x; l < k; l += kThreads) {
-    const long long t = S.terms[(long long)b * S.tmax + l];
-    s_term[l] = t;
-    s_v[l] = pool[t + h + j];
-  }
-  if (threadIdx.x == 0) atomicAdd(S.stat, (unsigned long long)h);
-  __syncthreads();
-  V *col = pool + pe;
-  unsigned *rm = S.rmask + S.rmask_off[b];
-  const int r0 = S.r0[b], c0 = S.c0[b];
-  const int dj = P.cperm[c0 + j];
-  double best = -1.0, ss = 0.0;
-  int bidx = 0x7fffffff;
-  if constexpr (NT == 1 && NS == 1) {
-    T y[18], nb[4];
-    load_q<T>(P.g.q, dj, y);
-    load_nj<T>(P.g.nj, dj, nb);
-    const int4 eb = P.elem[dj];
-    for (int r = threadIdx.x; r < h; r += kThreads) {
-      const int e = P.rperm[r0 + r];
-      V val;
-      if (touching(P.elem[e], eb)) {
-        val = entry<T, C, OP, HELM, 1, 1>(P, e, dj, S.stat + 1);
+  __shared__ unsigned long long s_ent[kWarps];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int pos = blockIdx.x * kWarps + wid;
+  unsigned long long ent = 0;
+  if (pos < nA) {
+    const int b = S.listA[pos];
+    const int h = S.h[b], w = S.w[b], i = S.cur[b];
+    const long long pe = row_slot(S, pos, b);
+    const V *row = static_cast<const V *>(S.pool) + pe + h;
+    const unsigned *cm = S.cmask + S.cmask_off[b];
+    double best = -1.0, ss = 0.0;
+    int bidx = 0x7fffffff;
+    for (int c = lane; c < w; c += 32) {
+      const V val = row[c];
+      const double a = N::abs(val);
+      ss += N::nrm(val);
+      if (!bit(cm, c) && a > best) { best = a; bidx = c; }
+    }
+    warp_argmax_sum(best, bidx, ss);
+    if (lane == 0) {
+      ent = (unsigned long long)w;
+      S.pend[b] = pe;
+      if (best <= 0.0) {
+        // residual row vanished: retire it to Z (hmatrix.py:334-338)
+        unsigned *rm = S.rmask + S.rmask_off[b];
+        set_bit(rm, i);
+        const int next = first_clear(rm, h);
+        if (next < 0) {
+          S.status[b] = ST_CONVERGED;
+          S.exhausted[b] = 1;
+        } else {
+          S.cur[b] = next;
+          const int q = atomicAdd(S.counts + 1, 1);
+          S.listA2[q] = b;
+          S.needA2[q] = make_longlong2(chunks_of(w), 0);
+        }
       } else {
-        T x[18], na[4], re[1][1], im[1][1];
-        load_q<T>(P.g.q, e, x);
-        load_nj<T>(P.g.nj, e, na);
-        regular_pair<T, OP, HELM, 1, 1>(P.R, x, y, na, nb, nullptr, nullptr, re, im);
-        val = N::mk(re[0][0], im[0][0]);
+        const V pv = row[bidx];
+        S.pcol[b] = bidx;
+        if constexpr (C) { S.piv[2 * b] = pv.re; S.piv[2 * b + 1] = pv.im; }
+        else { S.piv[2 * b] = pv; S.piv[2 * b + 1] = 0.0; }
+        S.rn2[b] = ss;
+        const int q = atomicAdd(S.counts, 1);
+        S.listC[q] = b;
+        S.needC[q] = chunks_of(h);
       }
-      for (int l = 0; l < k; ++l) val = N::fms(val, s_v[l], pool[s_term[l] + r]);
-      col[r] = val;
-      const double a = N::abs(val);
-      ss += N::nrm(val);
-      if (r != i && !bit(rm, r) && a > best) { best = a; bidx = r; }
-    }
-  } else {
-    for (int r = threadIdx.x; r < h; r += kThreads) {
-      const int di = P.rperm[r0 + r];
-      V val = entry<T, C, OP, HELM, NT, NS>(P, di, dj, S.stat + 1);
-      for (int l = 0; l < k; ++l) val = N::fms(val, s_v[l], pool[s_term[l] + r]);
-      col[r] = val;
-      const double a = N::abs(val);
-      ss += N::nrm(val);
-      if (r != i && !bit(rm, r) && a > best) { best = a; bidx = r; }
     }
   }
-  block_reduce(best, bidx, ss, s_bv, s_bi, s_ss);
-  const int next = best >= 0.0 ? bidx : -1;
+  if (lane == 0) s_ent[wid] = ent;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const double nu = sqrt(ss);
+    unsigned long long t = 0;
+    for (int k = 0; k < kWarps; ++k) t += s_ent[k];
+    if (t) atomicAdd(S.stat, t);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3d: column finalize, warp per block: |u||v| stopping test (two small
+// updates in a row stop, hmatrix.py:343-357), Frobenius update with the
+// cross terms (359-362), v = row / pivot, next row pivot argmax |u|.
+// ---------------------------------------------------------------------------
+template <typename T, bool C>
+__global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int nC) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  __shared__ unsigned long long s_ent[kWarps];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int pos = blockIdx.x * kWarps + wid;
+  unsigned long long ent = 0;
+  if (pos < nC) {
+    const int b = S.listC[pos];
+    const int h = S.h[b], w = S.w[b], i = S.cur[b], j = S.pcol[b], k = S.rank[b];
+    const long long pe = S.pend[b];
+    V *pool = static_cast<V *>(S.pool);
+    V *col = pool + pe;
+    V *row = pool + pe + h;
+    unsigned *rm = S.rmask + S.rmask_off[b];
+    double best = -1.0, ss = 0.0;
+    int bidx = 0x7fffffff;
+    for (int r = lane; r < h; r += 32) {
+      const V val = col[r];
+      const double a = N::abs(val);
+      ss += N::nrm(val);
+      if (r != i && !bit(rm, r) && a > best) { best = a; bidx = r; }
+    }
+    warp_argmax_sum(best, bidx, ss);
+    const int next = best >= 0.0 ? bidx : -1;
     const double pr = S.piv[2 * b], pim = S.piv[2 * b + 1];
+    const double nu = sqrt(ss);
     const double nv = sqrt(S.rn2[b]) / hypot(pr, pim);
     const double upd = nu * nv;
     const double n2 = S.norm2[b];
-    int accept = 1;
+    const int kmax_b = min(S.kmax_cfg, min(h, w));
+    ent = (unsigned long long)h;
     if (n2 > 0.0 && upd <= S.eps * sqrt(n2)) {
-      // negligible update: dropped; two in a row stop (hmatrix.py:347-357)
-      accept = 0;
-      S.resid[b] = upd / sqrt(n2);
-      const int sm = S.small[b] + 1;
-      S.small[b] = sm;
-      if (sm >= 2) {
-        S.status[b] = ST_CONVERGED;
-      } else {
-        set_bit(rm, i);
-        S.cur[b] = next;
-        S.listA2[atomicAdd(S.counts + 1, 1)] = b;
+      if (lane == 0) {
+        S.resid[b] = upd / sqrt(n2);
+        const int sm = S.small[b] + 1;
+        S.small[b] = sm;
+        if (sm >= 2) {
+          S.status[b] = ST_CONVERGED;
+        } else {
+          set_bit(rm, i);
+          if (next < 0) {
+            S.status[b] = ST_CONVERGED;
+            S.exhausted[b] = 1;
+          } else {
+            S.cur[b] = next;
+            const int q = atomicAdd(S.counts + 1, 1);
+            S.listA2[q] = b;
+            S.needA2[q] = make_longlong2(chunks_of(w), 0);  // reuse the pending slot
+          }
+        }
       }
-    }
-    s_accept = accept;
-    S.rn2[b] = upd;  // stash the update size for the accept path
-  }
-  __syncthreads();
-  if (!s_accept) return;
-  // cross terms sum_l Re(vdot(u_l, u) * vdot(v_l, v)) (hmatrix.py:359-361)
-  const V *row = pool + pe + h;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int l = 0; l < k; ++l) {
-    double ur = 0, ui = 0, vr = 0, vi = 0;
-    const V *ul = pool + s_term[l];
-    const V *vl = ul + h;
-    for (int r = threadIdx.x; r < h; r += kThreads) N::cdot(ur, ui, ul[r], col[r]);
-    for (int c = threadIdx.x; c < w; c += kThreads) N::cdot(vr, vi, vl[c], row[c]);
+    } else {
+      // accept: v = row / pivot in place, then the cross terms
+      V pv;
+      if constexpr (C) pv = V{(T)pr, (T)pim};
+      else pv = (T)pr;
+      for (int c = lane; c < w; c += 32) row[c] = N::div(row[c], pv);
+      __syncwarp();
+      double cross = 0.0;
+      const long long *tl = S.terms + (long long)b * S.tmax;
+      for (int l = 0; l < k; ++l) {
+        const V *ul = pool + tl[l];
+        const V *vl = ul + h;
+        double ur = 0, ui = 0, vr = 0, vi = 0;
+        for (int r = lane; r < h; r += 32) N::cdot(ur, ui, ul[r], col[r]);
+        for (int c = lane; c < w; c += 32) N::cdot(vr, vi, vl[c], row[c]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      ur += __shfl_xor_sync(0xffffffffu, ur, o);
-      ui += __shfl_xor_sync(0xffffffffu, ui, o);
-      vr += __shfl_xor_sync(0xffffffffu, vr, o);
-      vi += __shfl_xor_sync(0xffffffffu, vi, o);
-    }
-    if (lane == 0) {
-      s_dot[l][warp][0] = ur;
-      s_dot[l][warp][1] = ui;
-      s_dot[l][warp][2] = vr;
-      s_dot[l][warp][3] = vi;
-    }
-  }
-  __syncthreads();
-  const double pr = S.piv[2 * b], pim = S.piv[2 * b + 1];
-  if (threadIdx.x == 0) {
-    double cross = 0.0;
-    const double pd = pr * pr + pim * pim;
-    for (int l = 0; l < k; ++l) {
-      double ur = 0, ui = 0, vr = 0, vi = 0;
-      for (int q = 0; q < kWarps; ++q) {
-        ur += s_dot[l][q][0];
-        ui += s_dot[l][q][1];
-        vr += s_dot[l][q][2];
-        vi += s_dot[l][q][3];
+        for (int o = 16; o > 0; o >>= 1) {
+          ur += __shfl_xor_sync(0xffffffffu, ur, o);
+          ui += __shfl_xor_sync(0xffffffffu, ui, o);
+          vr += __shfl_xor_sync(0xffffffffu, vr, o);
+          vi += __shfl_xor_sync(0xffffffffu, vi, o);
+        }
+        cross += ur * vr - ui * vi;  // Re(vdot(u_l, u) * vdot(v_l, v))
       }
-      // vdot(v_l, v) = (sum conj(v_l) row) / pivot
-      const double dr = (vr * pr + vi * pim) / pd, di = (vi * pr - vr * pim) / pd;
-      cross += ur * dr - ui * di;
+      if (lane == 0) {
+        const double n2n = n2 + 2.0 * cross + upd * upd;
+        S.norm2[b] = n2n;
+        S.small[b] = 0;
+        S.terms[(long long)b * S.tmax + k] = pe;
+        S.pend[b] = -1;
+        S.rank[b] = k + 1;
+        set_bit(rm, i);
+        set_bit(S.cmask + S.cmask_off[b], j);
+        if (n2n > 0.0) {
+          S.resid[b] = upd / sqrt(n2n);
+          if (upd <= S.eps * sqrt(n2n)) S.small[b] = 1;
+        }
+        S.cur[b] = next;
+        // loop head of the next iteration (hmatrix.py:318-322)
+        if (k + 1 >= kmax_b) {
+          S.status[b] = ST_FALLBACK;
+        } else if (k + 1 >= S.tmax) {
+          S.status[b] = ST_OVERFLOW;
+        } else if (next < 0) {
+          S.status[b] = ST_CONVERGED;
+          S.exhausted[b] = 1;
+        } else {
+          const int q = atomicAdd(S.counts + 1, 1);
+          S.listA2[q] = b;
+          S.needA2[q] = make_longlong2(chunks_of(w), (long long)h + w);
+        }
+      }
     }
-    const double upd = S.rn2[b];
-    double n2 = S.norm2[b] + 2.0 * cross + upd * upd;
-    S.norm2[b] = n2;
-    S.small[b] = 0;
-    S.terms[(long long)b * S.tmax + k] = pe;
-    S.pend[b] = -1;
-    S.rank[b] = k + 1;
-    set_bit(rm, i);
-    set_bit(S.cmask + S.cmask_off[b], j);
-    if (n2 > 0.0) {
-      S.resid[b] = upd / sqrt(n2);
-      if (upd <= S.eps * sqrt(n2)) S.small[b] = 1;
-    }
-    S.cur[b] = next;
-    S.listA2[atomicAdd(S.counts + 1, 1)] = b;
   }
-  // v = row / pivot, in place (hmatrix.py:339)
-  V pv;
-  if constexpr (C) pv = V{(T)pr, (T)pim};
-  else pv = (T)pr;
-  V *rw = pool + pe + h;
-  for (int c = threadIdx.x; c < w; c += kThreads) rw[c] = N::div(rw[c], pv);
+  if (lane == 0) s_ent[wid] = ent;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int k = 0; k < kWarps; ++k) t += s_ent[k];
+    if (t) atomicAdd(S.stat, t);
+  }
 }
 
-__global__ void k_aca_init(AcaDev S, int n) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= n) return;
+// initial state; the wave-0 list is the size-sorted block order
+__global__ void k_aca_init(AcaDev S, int n, const int *order, int *listA, longlong2 *needA) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int b = order[q];
+  const int h = S.h[b], w = S.w[b];
+  listA[q] = b;
+  needA[q] = make_longlong2(chunks_of(w), (long long)h + w);
   S.rank[b] = 0;
   S.cur[b] = 0;
   S.small[b] = 0;
@@ -516,17 +606,29 @@ __global__ void k_aca_init(AcaDev S, int n) {
   S.norm2[b] = 0.0;
   S.resid[b] = INFINITY;
   S.pend[b] = -1;
-  // row mask padding bits preset (blocked), everything else clear
-  const int h = S.h[b], w = S.w[b];
   unsigned *rm = S.rmask + S.rmask_off[b];
   for (int k = 0; k < (h + 31) / 32; ++k) {
-    const int lo = k * 32;
-    const int valid = min(32, h - lo);
+    const int valid = min(32, h - k * 32);
     rm[k] = valid == 32 ? 0u : ~((1u << valid) - 1u);
   }
   unsigned *cm = S.cmask + S.cmask_off[b];
   for (int k = 0; k < (w + 31) / 32; ++k) cm[k] = 0u;
 }
+
+__global__ void k_zero_ll2(longlong2 *p, int n) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) p[q] = make_longlong2(0, 0);
+}
+__global__ void k_zero_ll(long long *p, int n) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) p[q] = 0;
+}
+
+struct SumLL2 {
+  __device__ __forceinline__ longlong2 operator()(const longlong2 &a, const longlong2 &b) const {
+    return make_longlong2(a.x + b.x, a.y + b.y);
+  }
+};
 
 // ---------------------------------------------------------------------------
 // K4: dense entries (near-field leaves and ACA fallback blocks).
@@ -664,6 +766,10 @@ struct hbem_hmat {
   int na = 0;
   std::vector<int> adm_leaf, ah, aw, ar0, ac0;
   int *d_order = nullptr, *listA = nullptr, *listA2 = nullptr;
+  longlong2 *needA = nullptr, *needA2 = nullptr, *scanA = nullptr;
+  long long *scanC = nullptr;
+  void *cub_tmp = nullptr;
+  size_t cub_bytes = 0;
   AcaDev S{};
   void *pool = nullptr;
   // near-field leaves
@@ -829,7 +935,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   }
   AcaDev &S = H->S;
   int tmax = d->rank_capacity > 0 ? d->rank_capacity : 64;
-  S.tmax = std::min(tmax, kTmaxSmem);
+  S.tmax = std::min(tmax, 256);
   S.kmax_cfg = d->k_max > 0 ? (int)std::min<int64_t>(d->k_max, 1 << 30) : (1 << 30);
   S.eps = d->epsilon;
   {
@@ -865,10 +971,33 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   HB_CHECK(dalloc(H, &S.cmask, cmw));
   HB_CHECK(dalloc(H, &H->listA, na));
   HB_CHECK(dalloc(H, &H->listA2, na));
-  HB_CHECK(dalloc(H, &S.listB, na));
+  HB_CHECK(dalloc(H, &S.listC, na));
+  HB_CHECK(dalloc(H, &H->needA, na));
+  HB_CHECK(dalloc(H, &H->needA2, na));
+  HB_CHECK(dalloc(H, &H->scanA, na));
+  HB_CHECK(dalloc(H, &S.needC, na));
+  HB_CHECK(dalloc(H, &H->scanC, na));
   HB_CHECK(dalloc(H, &S.counts, 4));
   HB_CHECK(dalloc(H, &S.stat, 4));
-  HB_CHECK(dalloc(H, &S.pool_top, 1));
+  {
+    // chunk map sized for the widest wave: every block's row and column
+    long long maxch = 0;
+    for (int q = 0; q < na; ++q)
+      maxch += std::max(chunks_of(H->ah[q]), chunks_of(H->aw[q]));
+    HB_CHECK(dalloc(H, &S.cmap, std::max<long long>(maxch, 1)));
+    HB_CHECK(dalloc(H, &S.jobs, na));
+    HB_CHECK(dalloc(H, (char **)&S.coef, (size_t)na * S.tmax * H->vbytes));
+  }
+  S.squeue_cap = 1 << 20;
+  HB_CHECK(dalloc(H, &S.squeue, S.squeue_cap));
+  {
+    size_t b1 = 0, b2 = 0;
+    HB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, b1, H->needA, H->scanA, SumLL2(),
+                                           std::max(na, 1)));
+    HB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, b2, S.needC, H->scanC, std::max(na, 1)));
+    H->cub_bytes = std::max(b1, b2);
+    HB_CHECK(dalloc(H, (char **)&H->cub_tmp, H->cub_bytes));
+  }
   // ---- near-field leaves --------------------------------------------------------
   const int nd = (int)H->den_leaf.size();
   H->nd = nd;
@@ -978,45 +1107,103 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   HB_CUDA(cudaEventRecord(H->ev[3], H->side));
   // ---- ACA waves ------------------------------------------------------------------
   HB_CUDA(cudaMemsetAsync(S.stat, 0, 32, st));
-  HB_CUDA(cudaMemsetAsync(S.pool_top, 0, 8, st));
   int waves = 0;
+  long long pool_top = 0;
   if (na > 0) {
-    k_aca_init<<<(na + 127) / 128, 128, 0, st>>>(S, na);
+    k_aca_init<<<(na + 127) / 128, 128, 0, st>>>(S, na, H->d_order, H->listA, H->needA);
     HB_CUDA(cudaGetLastError());
     ++launches;
-    HB_CUDA(cudaMemcpyAsync(H->listA, H->d_order, na * sizeof(int), cudaMemcpyDeviceToDevice,
-                            st));
     int nA = na;
     int *la = H->listA, *la2 = H->listA2;
-    int h_counts[2];
+    longlong2 *na_ = H->needA, *na2 = H->needA2;
+    // per wave: scan(row chunks, pool) -> int_row -> singular -> fin_row ->
+    // scan(col chunks) -> int_col -> singular -> fin_col; 2 host syncs
     while (nA > 0) {
       S.listA = la;
+      S.needA = na_;
+      S.scanA = H->scanA;
       S.listA2 = la2;
-      HB_CUDA(cudaMemsetAsync(S.counts, 0, 16, st));
+      S.needA2 = na2;
+      S.scanC = H->scanC;
       HB_CUDA(cudaEventRecord(H->ev[0], st));
+      size_t tb = H->cub_bytes;
+      HB_CUDA(cub::DeviceScan::InclusiveScan(H->cub_tmp, tb, na_, H->scanA, SumLL2(), nA, st));
+      longlong2 tot;
+      HB_CUDA(cudaMemcpyAsync(&tot, H->scanA + nA - 1, sizeof(tot), cudaMemcpyDeviceToHost, st));
+      HB_CUDA(cudaMemsetAsync(S.counts, 0, 16, st));
+      k_zero_ll<<<(nA + 255) / 256, 256, 0, st>>>(S.needC, nA);
+      k_zero_ll2<<<(nA + 255) / 256, 256, 0, st>>>(na2, nA);
+      HB_CUDA(cudaStreamSynchronize(st));
+      if (pool_top + tot.y > S.pool_cap)
+        return set_error(HBEM_ERR_CAPACITY,
+                         "ACA factor pool of %lld values exhausted at wave %d (need %lld more)",
+                         (long long)S.pool_cap, waves, (long long)(pool_top + tot.y - S.pool_cap));
+      S.pool_base = pool_top;
+      pool_top += tot.y;
+      const unsigned row_chunks = (unsigned)tot.x;
       int rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc,
                                                            auto NSc) -> int {
         constexpr int OP = decltype(OPc)::value;
         constexpr bool HH = decltype(Hc)::value != 0;
         constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
-        k_aca_row<T, C, OP, HH, NT, NS><<<nA, kThreads, 0, st>>>(P, S);
+        k_jobs<V><<<(nA + 127) / 128, 128, 0, st>>>(S, la, nA, 0, P.rperm, P.cperm);
         HB_CUDA(cudaGetLastError());
-        k_aca_col<T, C, OP, HH, NT, NS><<<nA, kThreads, 0, st>>>(P, S);
+        k_int<T, C, OP, HH, NT, NS, false><<<row_chunks, kThreads, 0, st>>>(P, S);
         HB_CUDA(cudaGetLastError());
+        if constexpr (NT == 1 && NS == 1) {
+          k_int_singular<T, C, OP, HH><<<148 * 4, kThreads, 0, st>>>(P, S, 0);
+          HB_CUDA(cudaGetLastError());
+        }
         return HBEM_OK;
       });
       if (rc != HBEM_OK) return rc;
-      launches += 2;
-      HB_CUDA(cudaEventRecord(H->ev[1], st));
-      HB_CUDA(cudaMemcpyAsync(h_counts, S.counts, 8, cudaMemcpyDeviceToHost, st));
+      k_fin_row<T, C><<<(nA + kWarps - 1) / kWarps, kThreads, 0, st>>>(S, nA);
+      HB_CUDA(cudaGetLastError());
+      size_t tb2 = H->cub_bytes;
+      HB_CUDA(cub::DeviceScan::InclusiveSum(H->cub_tmp, tb2, S.needC, H->scanC, nA, st));
+      int cnt[3];
+      long long col_chunks = 0;
+      HB_CUDA(cudaMemcpyAsync(cnt, S.counts, 12, cudaMemcpyDeviceToHost, st));
+      HB_CUDA(cudaMemcpyAsync(&col_chunks, H->scanC + nA - 1, 8, cudaMemcpyDeviceToHost, st));
+      HB_CUDA(cudaMemsetAsync(S.counts + 2, 0, 4, st));
       HB_CUDA(cudaStreamSynchronize(st));
+      if (cnt[2] > S.squeue_cap)
+        return set_error(HBEM_ERR_CAPACITY, "singular queue overflow (%d touching pairs)", cnt[2]);
+      const int nC = cnt[0];
+      if (nC > 0) {
+        rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc,
+                                                         auto NSc) -> int {
+          constexpr int OP = decltype(OPc)::value;
+          constexpr bool HH = decltype(Hc)::value != 0;
+          constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
+          k_jobs<V><<<(nC + 127) / 128, 128, 0, st>>>(S, S.listC, nC, 1, P.rperm, P.cperm);
+          HB_CUDA(cudaGetLastError());
+          k_int<T, C, OP, HH, NT, NS, true><<<(unsigned)col_chunks, kThreads, 0, st>>>(P, S);
+          HB_CUDA(cudaGetLastError());
+          if constexpr (NT == 1 && NS == 1) {
+            k_int_singular<T, C, OP, HH><<<148 * 4, kThreads, 0, st>>>(P, S, 1);
+            HB_CUDA(cudaGetLastError());
+          }
+          return HBEM_OK;
+        });
+        if (rc != HBEM_OK) return rc;
+        k_fin_col<T, C><<<(nC + kWarps - 1) / kWarps, kThreads, 0, st>>>(S, nC);
+        HB_CUDA(cudaGetLastError());
+      }
+      launches += (nt == 1 && ns == 1) ? 10 : 8;
+      HB_CUDA(cudaEventRecord(H->ev[1], st));
+      HB_CUDA(cudaMemcpyAsync(cnt, S.counts, 12, cudaMemcpyDeviceToHost, st));
+      HB_CUDA(cudaStreamSynchronize(st));
+      if (cnt[2] > S.squeue_cap)
+        return set_error(HBEM_ERR_CAPACITY, "singular queue overflow (%d touching pairs)", cnt[2]);
       float ms = 0.f;
       HB_CUDA(cudaEventElapsedTime(&ms, H->ev[0], H->ev[1]));
       ST.aca_kernel_ms += ms;
       ST.row_jobs += nA;
-      ST.col_jobs += h_counts[0];
-      nA = h_counts[1];
+      ST.col_jobs += nC;
+      nA = cnt[1];
       std::swap(la, la2);
+      std::swap(na_, na2);
       ++waves;
     }
   }
