@@ -1,0 +1,753 @@
+// Lock-step batched ACA over every admissible block (aca, hmatrix.py:271-382),
+// one phase = one launch family over all active blocks.
+//
+// Phase structure (row phase shown; the column phase is its mirror):
+//   select   deterministic stream compaction of the blocks that need a row
+//            job, in a static order sorted by column cluster: jobs that run
+//            over the same column cluster are adjacent ("groups");
+//   need     per job: pool values for a fresh pending term record, partial
+//            records (one per 32-wide tile), warp items (group heads only);
+//            one inclusive scan gives every offset;
+//   jobs     per job record + (group head, tile) warp items;
+//   integrate  one warp per item: lane l keeps the varying element of tile
+//            column 32 t + l in registers (P0) and walks every job of the
+//            group with the fixed element broadcast from shared memory; per
+//            entry: Galerkin integral (touching pairs: warp-cooperative
+//            Sauter-Schwab), residual update with the accepted terms
+//            (hmatrix.py:323-327 / 340-342), store; per tile: argmax over
+//            unmasked entries, sum |.|^2 and the dots with the factors the
+//            residual read (cross terms of the Frobenius update, 359-362);
+//   finalize one warp per job combines its tiles in fixed order: pivot,
+//            vanishing row (334-338), stopping test and norm update
+//            (343-370), next row pivot (301-314).
+// Every reduction runs in a fixed order, so payloads are bitwise
+// reproducible and independent of how blocks are split across GPUs.
+#pragma once
+#include <cub/cub.cuh>
+
+#include "hmat_common.cuh"
+
+namespace hb {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// state init, list selection, needs, jobs
+// ---------------------------------------------------------------------------
+static __global__ void k_aca_init(AcaDev S, int n) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  const int h = S.h[b], w = S.w[b];
+  S.rank[b] = 0;
+  S.cur[b] = 0;
+  S.small[b] = 0;
+  S.status[b] = ST_ACTIVE;
+  S.exhausted[b] = 0;
+  S.norm2[b] = 0.0;
+  S.resid[b] = INFINITY;
+  S.pend[b] = -1;
+  S.flagA[b] = 1;
+  S.flagC[b] = 0;
+  unsigned *rm = S.rmask + S.rmask_off[b];
+  for (int k = 0; k < (h + 31) / 32; ++k) {
+    const int valid = min(32, h - k * 32);
+    rm[k] = valid == 32 ? 0u : ~((1u << valid) - 1u);
+  }
+  unsigned *cm = S.cmask + S.cmask_off[b];
+  for (int k = 0; k < (w + 31) / 32; ++k) {
+    const int valid = min(32, w - k * 32);
+    cm[k] = valid == 32 ? 0u : ~((1u << valid) - 1u);
+  }
+}
+
+static __global__ void k_phase_flags(const unsigned char *flag, const int *order, int n,
+                              unsigned char *out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) out[q] = flag[order[q]];
+}
+
+template <int NC>
+__global__ void k_need(AcaDev S, int na, int col) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= na) return;
+  const int n = *S.nlist;
+  Need d{0, 0, 0};
+  if (p < n) {
+    const int b = S.list[p];
+    const int h = S.h[b], w = S.w[b], k = S.rank[b];
+    const int tiles = tiles_of(col ? h : w);
+    const int key = col ? S.rnode[b] : S.cnode[b];
+    bool head = p == 0;
+    if (!head) {
+      const int bp = S.list[p - 1];
+      head = key != (col ? S.rnode[bp] : S.cnode[bp]);
+    }
+    d.pool = (!col && S.pend[b] < 0) ? (long long)h + w + 1 : 0;
+    d.part = tiles * part_len(k, NC);
+    d.items = head ? tiles : 0;
+  }
+  S.need[p] = d;
+}
+
+template <typename T, bool C>
+__global__ void k_jobs(AcaDev S, int n, int col) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int b = S.list[p];
+  const Need sc = S.scan[p], nd = S.need[p];
+  Job J;
+  J.b = b;
+  J.h = S.h[b];
+  J.w = S.w[b];
+  J.k = S.rank[b];
+  const int r0 = S.r0[b], c0 = S.c0[b];
+  J.part = sc.part - nd.part;
+  if (!col) {
+    J.key = S.cnode[b];
+    J.fix = S.cur[b];
+    const long long pe = S.pend[b];
+    J.pe = pe >= 0 ? pe : S.pool_base + sc.pool - nd.pool;
+    J.nfix = r0 + J.fix;
+    J.vstart = c0;
+    J.nvar = J.w;
+    J.cur = J.fix;
+    S.rowpart[b] = J.part;
+  } else {
+    J.key = S.rnode[b];
+    J.fix = S.pcol[b];
+    J.pe = S.pend[b];
+    J.nfix = c0 + J.fix;
+    J.vstart = r0;
+    J.nvar = J.h;
+    J.cur = S.cur[b];
+  }
+  S.jobs[p] = J;
+  // first terms of the residual: record offsets and coefficients
+  if (J.k > 0) {
+    const V *pool = static_cast<const V *>(S.pool);
+    const long long *tl = S.terms + (long long)b * S.tmax;
+    const int fixo = col ? J.h + J.fix : J.fix;
+    long long *jt = S.jt + (long long)p * kFinRegs;
+    V *jc = static_cast<V *>(S.jc) + (long long)p * kFinRegs;
+    const int kk = min(J.k, kFinRegs);
+#pragma unroll
+    for (int l = 0; l < kFinRegs; ++l)
+      if (l < kk) {
+        const long long t = tl[l];
+        jt[l] = t;
+        jc[l] = N::div(pool[t + fixo], pool[t + J.h + J.w]);
+      }
+  }
+  if (nd.items) {
+    const long long base = sc.items - nd.items;
+    for (long long t = 0; t < nd.items; ++t) S.items[base + t] = make_int2(p, (int)t);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// warp helpers
+// ---------------------------------------------------------------------------
+template <typename V> __device__ __forceinline__ V shfl_v(V v, int src);
+template <> __device__ __forceinline__ double shfl_v<double>(double v, int src) {
+  return __shfl_sync(kFull, v, src);
+}
+template <> __device__ __forceinline__ float shfl_v<float>(float v, int src) {
+  return __shfl_sync(kFull, v, src);
+}
+template <> __device__ __forceinline__ Cx<double> shfl_v<Cx<double>>(Cx<double> v, int src) {
+  return Cx<double>{__shfl_sync(kFull, v.re, src), __shfl_sync(kFull, v.im, src)};
+}
+template <> __device__ __forceinline__ Cx<float> shfl_v<Cx<float>>(Cx<float> v, int src) {
+  return Cx<float>{__shfl_sync(kFull, v.re, src), __shfl_sync(kFull, v.im, src)};
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Transposed warp reduction of 8 per-lane values: after 9 shuffles lane l
+// holds the warp total of value index l >> 2 (the halving exchange keeps
+// half of the values per step, then two butterfly steps finish).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double tr_reduce8(const double (&v)[8], int lane) {
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+  double a[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double send = h16 ? v[i] : v[i + 4];
+    const double keep = h16 ? v[i + 4] : v[i];
+    a[i] = keep + __shfl_xor_sync(kFull, send, 16);
+  }
+  double b[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double send = h8 ? a[i] : a[i + 2];
+    const double keep = h8 ? a[i + 2] : a[i];
+    b[i] = keep + __shfl_xor_sync(kFull, send, 8);
+  }
+  double c;
+  {
+    const double send = h4 ? b[0] : b[1];
+    const double keep = h4 ? b[1] : b[0];
+    c = keep + __shfl_xor_sync(kFull, send, 4);
+  }
+  c += __shfl_xor_sync(kFull, c, 2);
+  c += __shfl_xor_sync(kFull, c, 1);
+  return c;
+}
+
+// cp.async (LDGSTS) of one value into shared memory: the residual factor
+// prefetch costs no registers while the quadrature runs
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+// job view staged in shared memory by the integration kernels
+struct JobS {
+  long long pe;     // pending record
+  long long part;   // first tile record
+  long long mofs;   // mask word base of the varying side
+  int b, h, w, k, fix, cur;
+};
+
+// ---------------------------------------------------------------------------
+// ACA residual epilogue of one (job, tile) — shared by the P0 and linear-space
+// integration kernels.  f[l] (l < min(k, 8)) are the factor values of the
+// first terms at this lane's entry, prefetched before the integral; c[l] the
+// coefficients (row phase u_l[i] / p_l, column phase r_l[j] / p_l).
+//   row:    val = A(i, c) - sum_l u_l[i] v_l[c]   (hmatrix.py:323-327)
+//   column: val = A(r, j) - sum_l v_l[j] u_l[r]   (hmatrix.py:340-342)
+// Writes the residual into the pending record and the tile record
+// [best |val| over unmasked, its index, sum |val|^2, vdot(f_l, val) ...].
+// ---------------------------------------------------------------------------
+template <typename T, bool C, bool COL>
+__device__ __forceinline__ void aca_epi(const AcaDev &S, const JobS &J, const V_t<T, C> *cs,
+                                        int t, int lane, bool valid, V_t<T, C> val,
+                                        const V_t<T, C> *fb, unsigned m) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  constexpr int NC = N::NC;
+  V *pool = static_cast<V *>(S.pool);
+  const int idx = t * 32 + lane;
+  const int k = J.k, kk = min(k, kFinRegs);
+  const int ro = COL ? 0 : J.h;
+  // f_l at this lane's entry: fb[l * 32 + lane] (valid lanes only)
+#pragma unroll
+  for (int l = 0; l < kFinRegs; ++l)
+    if (l < kk && valid) val = N::fms(val, cs[l], fb[l * 32 + lane]);
+  // terms beyond the register batch (late waves of high-rank blocks)
+  const long long *tl = S.terms + (long long)J.b * S.tmax;
+  const int fixo = COL ? J.h + J.fix : J.fix;
+  for (int l = kFinRegs; l < k; ++l) {
+    const long long tb = tl[l];
+    const V c = N::div(pool[tb + fixo], pool[tb + J.h + J.w]);
+    if (valid) val = N::fms(val, c, pool[tb + ro + idx]);
+  }
+  if (valid) pool[J.pe + (COL ? 0 : J.h) + idx] = val;
+  // tile statistics
+  const bool masked = ((m >> lane) & 1u) || (COL && idx == J.cur);
+  double best = (valid && !masked) ? N::abs(val) : -1.0;
+  int bidx = (valid && !masked) ? idx : 0x7fffffff;
+  double ss = valid ? N::nrm(val) : 0.0;
+  warp_argmax_sum(best, bidx, ss);
+  double *rec = S.part + J.part + (long long)t * part_len(k, NC);
+  if (lane == 0) {
+    rec[0] = best;
+    rec[1] = (double)bidx;
+    rec[2] = ss;
+  }
+  // dots vdot(f_l, val) of the register batch: transposed reduction
+  if (kk > 0) {
+    double dr[8], di[8];
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      dr[l] = 0.0;
+      di[l] = 0.0;
+      if (l < kk && valid) N::cdot(dr[l], di[l], fb[l * 32 + lane], val);
+    }
+    const double sr = tr_reduce8(dr, lane);
+    const double si = C ? tr_reduce8(di, lane) : 0.0;
+    const int l = lane >> 2;
+    if ((lane & 3) == 0 && l < kk) {
+      rec[3 + l * NC] = sr;
+      if (C) rec[3 + l * NC + 1] = si;
+    }
+  }
+  for (int l = kFinRegs; l < k; ++l) {
+    const long long tb = tl[l];
+    double dr = 0.0, di = 0.0;
+    if (valid) N::cdot(dr, di, pool[tb + ro + idx], val);
+    dr = warp_sum_d(dr);
+    if (C) di = warp_sum_d(di);
+    if (lane == 0) {
+      rec[3 + l * NC] = dr;
+      if (C) rec[3 + l * NC + 1] = di;
+    }
+  }
+}
+
+// stage job p (lane-level) into shared memory; returns false past the group
+template <typename T, bool C, bool COL>
+__device__ __forceinline__ bool stage_job(const AcaDev &S, int p, int n, int key0, JobS &js,
+                                          long long (&jt)[kFinRegs], V_t<T, C> (&jc)[kFinRegs]) {
+  if (p >= n) return false;
+  const Job J = S.jobs[p];
+  if (J.key != key0) return false;
+  js.pe = J.pe;
+  js.part = J.part;
+  js.mofs = COL ? S.rmask_off[J.b] : S.cmask_off[J.b];
+  js.b = J.b;
+  js.h = J.h;
+  js.w = J.w;
+  js.k = J.k;
+  js.fix = J.fix;
+  js.cur = J.cur;
+  const int kk = min(J.k, kFinRegs);
+  const long long *gjt = S.jt + (long long)p * kFinRegs;
+  const V_t<T, C> *gjc = static_cast<const V_t<T, C> *>(S.jc) + (long long)p * kFinRegs;
+#pragma unroll
+  for (int l = 0; l < kFinRegs; ++l)
+    if (l < kk) {
+      jt[l] = gjt[l];
+      jc[l] = gjc[l];
+    }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// K3 (P0): one warp per (group head, 32-wide tile).  Lane l keeps the varying
+// element of tile column 32 t + l in registers and walks every job of the
+// group; fixed elements, job views and residual coefficients of kSeg jobs at
+// a time are staged in shared memory and broadcast.  The residual factor
+// values of a job are loaded before its integral so their latency hides
+// behind the quadrature.
+// ---------------------------------------------------------------------------
+template <typename T, bool C, int OP, bool HELM, bool COL>
+__global__ void __launch_bounds__(kThreads, 4) k_aca_p0(Prob<T> P, AcaDev S, int n,
+                                                        long long n_items) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  constexpr int kSeg = sizeof(V) > 8 ? 8 : 16;  // jobs staged per segment (48 KB static smem)
+  __shared__ ElemRec<T> sr[kWarps][kSeg];
+  __shared__ JobS sj[kWarps][kSeg];
+  __shared__ long long sjt[kWarps][kSeg][kFinRegs];
+  __shared__ V sjc[kWarps][kSeg][kFinRegs];
+  __shared__ V fbuf[kWarps][2][kFinRegs * 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long item = (long long)blockIdx.x * kWarps + wid;
+  if (item >= n_items) return;
+  const int2 it = S.items[item];
+  const int p0 = it.x, t = it.y;
+  const Job J0 = S.jobs[p0];
+  const int key0 = J0.key, vstart = J0.vstart, nvar = J0.nvar;
+  const int idx = t * 32 + lane;
+  const bool valid = idx < nvar;
+  ElemRec<T> my;
+  load_rec<T>(COL ? P.trec : P.srec, vstart + (valid ? idx : nvar - 1), my);
+  const V *pool = static_cast<const V *>(S.pool);
+  const unsigned *masks = COL ? S.rmask : S.cmask;
+  unsigned long long nent = 0, nsing = 0;
+  for (int seg = p0;; seg += kSeg) {
+    bool ok = false;
+    if (lane < kSeg) {
+      JobS js;
+      long long jt[kFinRegs];
+      V jc[kFinRegs];
+      ok = stage_job<T, C, COL>(S, seg + lane, n, key0, js, jt, jc);
+      if (ok) {
+        sj[wid][lane] = js;
+#pragma unroll
+        for (int l = 0; l < kFinRegs; ++l)
+          if (l < min(js.k, kFinRegs)) {
+            sjt[wid][lane][l] = jt[l];
+            sjc[wid][lane][l] = jc[l];
+          }
+        ElemRec<T> r;
+        load_rec<T>(COL ? P.srec : P.trec, (COL ? S.c0[js.b] : S.r0[js.b]) + js.fix, r);
+        sr[wid][lane] = r;
+      }
+    }
+    const unsigned okm = __ballot_sync(kFull, ok) | ~((1u << kSeg) - 1u);
+    const int nseg = okm == kFull ? kSeg : __ffs(~okm) - 1;
+    __syncwarp();
+    // jobs in pairs: two independent quadrature chains share the lane's points
+    for (int s = 0; s < nseg; s += 2) {
+      const int nj = s + 1 < nseg ? 2 : 1;
+      unsigned m[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (u < nj) {
+          const JobS &J = sj[wid][s + u];
+          const int kk = min(J.k, kFinRegs);
+          const int ro = COL ? 0 : J.h;
+#pragma unroll
+          for (int l = 0; l < kFinRegs; ++l)
+            if (l < kk && valid)
+              cp_async<sizeof(V)>(&fbuf[wid][u][l * 32 + lane], pool + sjt[wid][s + u][l] + ro + idx);
+          m[u] = masks[J.mofs + t];
+        }
+      }
+      V val[2];
+      if (nj == 2) {
+        const ElemRec<T> *const F2[2] = {&sr[wid][s], &sr[wid][s + 1]};
+        p0_pairs_fx<T, C, OP, HELM, !COL, 2>(P.R, F2, my.q, my.n, val);
+      } else {
+        const ElemRec<T> *const F1[1] = {&sr[wid][s]};
+        V v1[1];
+        p0_pairs_fx<T, C, OP, HELM, !COL, 1>(P.R, F1, my.q, my.n, v1);
+        val[0] = v1[0];
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (u < nj) {
+          const int4 fev = sr[wid][s + u].ev;
+          unsigned tm = __ballot_sync(kFull, valid && touching4(my.ev, fev));
+          while (tm) {
+            const int src = __ffs(tm) - 1;
+            tm &= tm - 1;
+            const int ev = __shfl_sync(kFull, my.ev.w, src);
+            const double2 sv =
+                singular_warp<OP, HELM>(P.G64, COL ? ev : fev.w, COL ? fev.w : ev);
+            if (lane == src) val[u] = N::mk((T)sv.x, (T)sv.y);
+            ++nsing;
+          }
+        }
+      }
+      cp_async_wait_all();
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (u < nj)
+          aca_epi<T, C, COL>(S, sj[wid][s + u], sjc[wid][s + u], t, lane, valid, val[u],
+                             fbuf[wid][u], m[u]);
+    }
+    nent += valid ? nseg : 0;
+    __syncwarp();
+    if (nseg < kSeg) break;
+  }
+  nent = (unsigned long long)__reduce_add_sync(kFull, (unsigned)nent);
+  if (lane == 0) {
+    atomicAdd(S.stat, nent);
+    if (nsing) atomicAdd(S.stat + 1, nsing);
+  }
+}
+
+// K3 (linear spaces): entries summed over the carrying element pairs
+template <typename T, bool C, int OP, bool HELM, int NT, int NS, bool COL>
+__global__ void __launch_bounds__(kThreads) k_aca_gen(Prob<T> P, AcaDev S, int n,
+                                                      long long n_items) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  __shared__ JobS sj[kWarps];
+  __shared__ V sjc[kWarps][kFinRegs];
+  __shared__ V fbuf[kWarps][kFinRegs * 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long item = (long long)blockIdx.x * kWarps + wid;
+  if (item >= n_items) return;
+  const int2 it = S.items[item];
+  const int p0 = it.x, t = it.y;
+  const Job J0 = S.jobs[p0];
+  const int key0 = J0.key;
+  const int idx = t * 32 + lane;
+  const bool valid = idx < J0.nvar;
+  const int vdof = valid ? (COL ? P.rperm : P.cperm)[J0.vstart + idx] : 0;
+  const V *pool = static_cast<const V *>(S.pool);
+  const unsigned *masks = COL ? S.rmask : S.cmask;
+  unsigned long long nent = 0;
+  for (int p = p0;; ++p) {
+    bool ok = false;
+    if (lane == 0) {
+      JobS js;
+      long long jt[kFinRegs];
+      V jc[kFinRegs];
+      ok = stage_job<T, C, COL>(S, p, n, key0, js, jt, jc);
+      if (ok) {
+        sj[wid] = js;
+#pragma unroll
+        for (int l = 0; l < kFinRegs; ++l)
+          if (l < min(js.k, kFinRegs)) sjc[wid][l] = jc[l];
+      }
+    }
+    if (!__shfl_sync(kFull, ok, 0)) break;
+    __syncwarp();
+    const JobS J = sj[wid];
+    const int kk = min(J.k, kFinRegs);
+    const int ro = COL ? 0 : J.h;
+    const long long *gjt = S.jt + (long long)p * kFinRegs;
+#pragma unroll
+    for (int l = 0; l < kFinRegs; ++l)
+      if (l < kk && valid) cp_async<sizeof(V)>(&fbuf[wid][l * 32 + lane], pool + gjt[l] + ro + idx);
+    const unsigned m = masks[J.mofs + t];
+    const int fdof = COL ? P.cperm[S.c0[J.b] + J.fix] : P.rperm[S.r0[J.b] + J.fix];
+    V val = N::zero();
+    if (valid)
+      val = COL ? entry<T, C, OP, HELM, NT, NS>(P, vdof, fdof, S.stat + 1)
+                : entry<T, C, OP, HELM, NT, NS>(P, fdof, vdof, S.stat + 1);
+    cp_async_wait_all();
+    aca_epi<T, C, COL>(S, J, sjc[wid], t, lane, valid, val, fbuf[wid], m);
+    nent += valid ? 1 : 0;
+    __syncwarp();
+  }
+  nent = (unsigned long long)__reduce_add_sync(kFull, (unsigned)nent);
+  if (lane == 0) atomicAdd(S.stat, nent);
+}
+
+// ---------------------------------------------------------------------------
+// finalize (thread per job; tiles combined in fixed tile order)
+//
+// Term records are [u (h) | r (w) | p]: the residual row r is kept unscaled
+// and its pivot p stored behind it, v = r / p is applied where v is read
+// (residual coefficients, cross terms, payload packing).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void combine_tiles(const double *rec, int nt, long long RL,
+                                              double &best, int &bidx, double &ss) {
+  best = -1.0;
+  bidx = 0x7fffffff;
+  ss = 0.0;
+  for (int t = 0; t < nt; ++t) {
+    const double *r = rec + t * RL;
+    const double a = r[0];
+    const int ix = (int)r[1];
+    if (better(a, ix, best, bidx)) { best = a; bidx = ix; }
+    ss += r[2];
+  }
+}
+
+// row finalize: column pivot (hmatrix.py:329-332) or vanishing row (334-338);
+// the dot totals over the tiles are kept in tile 0 for the column finalize
+template <typename T, bool C>
+__global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int n) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  constexpr int NC = N::NC;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const Job J = S.jobs[p];
+  const int b = J.b, h = J.h, w = J.w, i = J.fix, k = J.k;
+  const int nt = tiles_of(w);
+  const long long RL = part_len(k, NC);
+  double *rec = S.part + J.part;
+  double best, ss;
+  int bidx;
+  combine_tiles(rec, nt, RL, best, bidx, ss);
+  S.pend[b] = J.pe;
+  if (best <= 0.0) {
+    unsigned *rm = S.rmask + S.rmask_off[b];
+    set_bit(rm, i);
+    const int next = first_clear(rm, h);
+    if (next < 0) {
+      S.status[b] = ST_CONVERGED;
+      S.exhausted[b] = 1;
+    } else {
+      S.cur[b] = next;
+      S.flagA[b] = 1;
+    }
+    return;
+  }
+  for (int l = 0; l < k * NC; ++l) {
+    double s = 0.0;
+    for (int t = 0; t < nt; ++t) s += rec[t * RL + 3 + l];
+    rec[3 + l] = s;
+  }
+  V *pool = static_cast<V *>(S.pool);
+  const V pv = pool[J.pe + h + bidx];
+  pool[J.pe + h + w] = pv;
+  S.pcol[b] = bidx;
+  S.piv[2 * b] = (double)N::re(pv);
+  S.piv[2 * b + 1] = (double)N::im(pv);
+  S.rn2[b] = ss;
+  S.flagC[b] = 1;
+}
+
+// column finalize: stopping test (343-357), Frobenius update with the cross
+// terms (359-362), next row pivot (301-314)
+template <typename T, bool C>
+__global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  constexpr int NC = N::NC;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const Job J = S.jobs[p];
+  const int b = J.b, h = J.h, w = J.w, j = J.fix, k = J.k, i = J.cur;
+  const int ntc = tiles_of(h);
+  const long long RL = part_len(k, NC);
+  const double *crec = S.part + J.part;
+  double best, ss;
+  int bidx;
+  combine_tiles(crec, ntc, RL, best, bidx, ss);
+  const int next = best >= 0.0 ? bidx : -1;
+  const double pr = S.piv[2 * b], pim = S.piv[2 * b + 1];
+  const double nu = sqrt(ss);
+  const double nv = sqrt(S.rn2[b]) / hypot(pr, pim);
+  const double upd = nu * nv;
+  const double n2 = S.norm2[b];
+  const int kmax_b = min(S.kmax_cfg, min(h, w));
+  unsigned *rm = S.rmask + S.rmask_off[b];
+  if (n2 > 0.0 && upd <= S.eps * sqrt(n2)) {
+    S.resid[b] = upd / sqrt(n2);
+    const int sm = S.small[b] + 1;
+    S.small[b] = sm;
+    if (sm >= 2) {
+      S.status[b] = ST_CONVERGED;
+    } else {
+      set_bit(rm, i);
+      if (next < 0) {
+        S.status[b] = ST_CONVERGED;
+        S.exhausted[b] = 1;
+      } else {
+        S.cur[b] = next;
+        S.flagA[b] = 1;  // the pending record is reused
+      }
+    }
+    return;
+  }
+  // cross terms Re(vdot(u_l, u) vdot(v_l, v)) with v_l = r_l / p_l, v = r / p:
+  // vdot(v_l, v) = vdot(r_l, r) / (conj(p_l) p)
+  const V *pool = static_cast<const V *>(S.pool);
+  const double *rdots = S.rpart + S.rowpart[b] + 3;
+  const long long *tl = S.terms + (long long)b * S.tmax;
+  double cross = 0.0;
+  for (int l = 0; l < k; ++l) {
+    double ur = 0.0, ui = 0.0;
+    for (int t = 0; t < ntc; ++t) {
+      ur += crec[t * RL + 3 + (long long)l * NC];
+      if (C) ui += crec[t * RL + 3 + (long long)l * NC + 1];
+    }
+    const double vr = rdots[(long long)l * NC], vi = C ? rdots[(long long)l * NC + 1] : 0.0;
+    const V pl = pool[tl[l] + h + w];
+    const double plr = (double)N::re(pl), pli = (double)N::im(pl);
+    const double dr = plr * pr + pli * pim, di = plr * pim - pli * pr;  // conj(p_l) p
+    double qr, qi;
+    if (C) {
+      const double d = dr * dr + di * di;
+      qr = (vr * dr + vi * di) / d;
+      qi = (vi * dr - vr * di) / d;
+    } else {
+      qr = vr / dr;
+      qi = 0.0;
+    }
+    cross += ur * qr - ui * qi;
+  }
+  const double n2n = n2 + 2.0 * cross + upd * upd;
+  S.norm2[b] = n2n;
+  S.small[b] = 0;
+  S.terms[(long long)b * S.tmax + k] = J.pe;
+  S.pend[b] = -1;
+  S.rank[b] = k + 1;
+  set_bit(rm, i);
+  set_bit(S.cmask + S.cmask_off[b], j);
+  if (n2n > 0.0) {
+    S.resid[b] = upd / sqrt(n2n);
+    if (upd <= S.eps * sqrt(n2n)) S.small[b] = 1;
+  }
+  S.cur[b] = next;
+  // loop head of the next iteration (hmatrix.py:318-322)
+  if (k + 1 >= kmax_b) {
+    S.status[b] = ST_FALLBACK;
+  } else if (k + 1 >= S.tmax) {
+    S.status[b] = ST_OVERFLOW;
+  } else if (next < 0) {
+    S.status[b] = ST_CONVERGED;
+    S.exhausted[b] = 1;
+  } else {
+    S.flagA[b] = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+template <typename T, bool C>
+int aca_init(const Prob<T> &, AcaDev &S, int na, cudaStream_t st) {
+  if (na <= 0) return HBEM_OK;
+  k_aca_init<<<(na + 127) / 128, 128, 0, st>>>(S, na);
+  HB_CUDA(cudaGetLastError());
+  return HBEM_OK;
+}
+
+template <typename T, bool C>
+int aca_select(const Prob<T> &, AcaDev &S, const PhaseArgs &A, cudaStream_t st) {
+  constexpr int NC = Num<T, C>::NC;
+  const int na = A.na;
+  unsigned char *flags = A.col_phase ? S.flagC : S.flagA;
+  k_phase_flags<<<(na + 255) / 256, 256, 0, st>>>(flags, A.order, na,
+                                                   reinterpret_cast<unsigned char *>(A.sel_tmp));
+  HB_CUDA(cudaGetLastError());
+  size_t tb = A.cub_bytes;
+  HB_CUDA(cub::DeviceSelect::Flagged(A.cub_tmp, tb, A.order,
+                                     reinterpret_cast<unsigned char *>(A.sel_tmp),
+                                     const_cast<int *>(S.list), const_cast<int *>(S.nlist), na,
+                                     st));
+  if (!A.col_phase) {
+    // the row phase consumes the row flags; fin_row/fin_col set them again
+    HB_CUDA(cudaMemsetAsync(S.flagA, 0, na, st));
+    HB_CUDA(cudaMemsetAsync(S.flagC, 0, na, st));
+  }
+  k_need<NC><<<(na + 255) / 256, 256, 0, st>>>(S, na, A.col_phase);
+  HB_CUDA(cudaGetLastError());
+  tb = A.cub_bytes;
+  HB_CUDA(cub::DeviceScan::InclusiveScan(A.cub_tmp, tb, S.need, S.scan, SumNeed(), na, st));
+  return HBEM_OK;
+}
+
+inline size_t aca_cub_bytes_impl(int na) {
+  size_t b1 = 0, b2 = 0;
+  cub::DeviceSelect::Flagged(nullptr, b1, (const int *)nullptr, (const unsigned char *)nullptr,
+                             (int *)nullptr, (int *)nullptr, std::max(na, 1));
+  cub::DeviceScan::InclusiveScan(nullptr, b2, (const Need *)nullptr, (Need *)nullptr, SumNeed(),
+                                 std::max(na, 1));
+  return std::max(b1, b2);
+}
+
+template <typename T, bool C>
+int aca_phase(const Prob<T> &P, AcaDev &S, const PhaseArgs &A, int op, bool helm, int nt, int ns,
+              int n, long long n_items, cudaStream_t st) {
+  if (n <= 0) return HBEM_OK;
+  const int col = A.col_phase;
+  k_jobs<T, C><<<(n + 127) / 128, 128, 0, st>>>(S, n, col);
+  HB_CUDA(cudaGetLastError());
+  if (n_items > 0) {
+    const unsigned grid = (unsigned)((n_items + kWarps - 1) / kWarps);
+    int rc = dispatch_op(op, helm, nt, ns, [&](auto OPc, auto Hc, auto NTc, auto NSc) -> int {
+      constexpr int OP = decltype(OPc)::value;
+      constexpr bool HH = decltype(Hc)::value != 0;
+      constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
+      if constexpr (HH == C) {
+        if constexpr (NT == 1 && NS == 1) {
+          if (col) k_aca_p0<T, C, OP, HH, true><<<grid, kThreads, 0, st>>>(P, S, n, n_items);
+          else k_aca_p0<T, C, OP, HH, false><<<grid, kThreads, 0, st>>>(P, S, n, n_items);
+        } else {
+          if (col)
+            k_aca_gen<T, C, OP, HH, NT, NS, true><<<grid, kThreads, 0, st>>>(P, S, n, n_items);
+          else
+            k_aca_gen<T, C, OP, HH, NT, NS, false><<<grid, kThreads, 0, st>>>(P, S, n, n_items);
+        }
+        HB_CUDA(cudaGetLastError());
+        return HBEM_OK;
+      } else {
+        return set_error(HBEM_ERR_KERNEL, "value type does not match the equation");
+      }
+    });
+    if (rc != HBEM_OK) return rc;
+  }
+  const unsigned fgrid = (unsigned)((n + kThreads - 1) / kThreads);
+  if (col) k_fin_col<T, C><<<fgrid, kThreads, 0, st>>>(S, n);
+  else k_fin_row<T, C><<<fgrid, kThreads, 0, st>>>(S, n);
+  HB_CUDA(cudaGetLastError());
+  return HBEM_OK;
+}
+
+}  // namespace hb

@@ -1,13 +1,14 @@
 // Device H-matrix assembly: near-field dense leaves + lock-step batched ACA
 // over every admissible leaf (assemble_hmatrix, hmatrix.py:759-811).
 //
-// The reference runs aca() (hmatrix.py:271-382) block by block on the host,
-// each step issuing one row job and one column job (hmatrix.py:625-672).
-// Here all admissible blocks advance together in "waves": one launch
-// evaluates the next ACA row of every active block (one CTA per block:
-// integrals + residual update + column pivot search), a second launch the
-// pivot column (integrals + residual + stopping test + Frobenius update +
-// next row pivot).  Per-block decisions follow aca() exactly:
+// This translation unit holds the host orchestration (setup = partition
+// upload and index structures, execute = one full assembly), the generic
+// dense-entry kernels (linear spaces, ACA fallback blocks) and payload
+// packing.  The ACA wave kernels live in aca_impl.cuh, the P0 near-field
+// kernels in near_impl.cuh (instantiated per precision in kern_f64.cu /
+// kern_f32.cu).
+//
+// Per-block decisions follow aca() (hmatrix.py:271-382) exactly:
 //   * first row = lowest unused index; next row = argmax |u_k| over rows not
 //     yet used or retired (first index on ties, hmatrix.py:301-314);
 //   * column pivot = argmax |residual row| over unused columns (329-332);
@@ -30,622 +31,15 @@
 #include <numeric>
 #include <vector>
 
-#include <cub/cub.cuh>
-
-#include "hbem_internal.h"
+#include "hmat_common.cuh"
 
 namespace hb {
 
-// ---------------------------------------------------------------------------
-// value arithmetic (real T or complex as (re, im) pairs, numpy layout)
-// ---------------------------------------------------------------------------
-template <typename T> struct Cx { T re, im; };
-
-template <typename T, bool C> struct Num;
-template <typename T> struct Num<T, false> {
-  using V = T;
-  __device__ static V mk(T r, T) { return r; }
-  __device__ static V fms(V a, V b, V c) { return a - b * c; }
-  __device__ static double abs(V a) { return fabs((double)a); }
-  __device__ static double nrm(V a) { return (double)a * (double)a; }
-  __device__ static void cdot(double &re, double &, V a, V b) { re += (double)a * (double)b; }
-  __device__ static V div(V a, V b) { return a / b; }
-  __device__ static V zero() { return T(0); }
-  __device__ static V fma_acc(V acc, V a, V b) { return acc + a * b; }
-};
-template <typename T> struct Num<T, true> {
-  using V = Cx<T>;
-  __device__ static V mk(T r, T i) { return V{r, i}; }
-  __device__ static V fms(V a, V b, V c) {
-    return V{a.re - (b.re * c.re - b.im * c.im), a.im - (b.re * c.im + b.im * c.re)};
-  }
-  __device__ static double abs(V a) { return hypot((double)a.re, (double)a.im); }
-  __device__ static double nrm(V a) {
-    return (double)a.re * (double)a.re + (double)a.im * (double)a.im;
-  }
-  __device__ static void cdot(double &re, double &im, V a, V b) {  // conj(a) b
-    re += (double)a.re * (double)b.re + (double)a.im * (double)b.im;
-    im += (double)a.re * (double)b.im - (double)a.im * (double)b.re;
-  }
-  __device__ static V div(V a, V b) {
-    const T d = b.re * b.re + b.im * b.im;
-    return V{(a.re * b.re + a.im * b.im) / d, (a.im * b.re - a.re * b.im) / d};
-  }
-  __device__ static V zero() { return V{T(0), T(0)}; }
-  __device__ static V fma_acc(V acc, V a, V b) {
-    return V{acc.re + (a.re * b.re - a.im * b.im), acc.im + (a.re * b.im + a.im * b.re)};
-  }
-};
-
-// ---------------------------------------------------------------------------
-// problem view: geometry + DOF maps
-// ---------------------------------------------------------------------------
-template <typename T> struct Prob {
-  Geo<T> g;
-  RuleTab<T> R;
-  Geo64 G64;
-  const int4 *elem;
-  const int *rperm, *cperm;  // tree position -> DOF
-  // DOF -> (element, local) incidence CSR (linear spaces)
-  const int *tptr, *tel;
-  const signed char *tloc;
-  const int *sptr, *sel;
-  const signed char *sloc;
-};
-
-// block of one element pair (any adjacency), thread-level
-template <typename T, int OP, bool HELM, int NT, int NS>
-__device__ __forceinline__ void pair_block(const Prob<T> &P, int e, int f, T (&re)[NT][NS],
-                                           T (&im)[NT][NS], unsigned long long *nsing) {
-  if (touching(P.elem[e], P.elem[f])) {
-    double dr[NT][NS], di[NT][NS];
-    singular_local<OP, HELM, NT, NS, 1>(P.G64, e, f, dr, di);
-#pragma unroll
-    for (int i = 0; i < NT; ++i)
-#pragma unroll
-      for (int j = 0; j < NS; ++j) { re[i][j] = (T)dr[i][j]; im[i][j] = (T)di[i][j]; }
-    if (nsing) atomicAdd(nsing, 1ull);
-    return;
-  }
-  T x[18], y[18], na[4], nb[4];
-  load_q<T>(P.g.q, e, x);
-  load_q<T>(P.g.q, f, y);
-  load_nj<T>(P.g.nj, e, na);
-  load_nj<T>(P.g.nj, f, nb);
-  const T *ca = nullptr, *cb = nullptr;
-  if (OP == HBEM_HYPS) { ca = P.g.curl + 9 * (int64_t)e; cb = P.g.curl + 9 * (int64_t)f; }
-  regular_pair<T, OP, HELM, NT, NS>(P.R, x, y, na, nb, ca, cb, re, im);
-}
-
-// Matrix entry (test DOF di, trial DOF dj): sum over the element pairs that
-// carry both DOFs, in (test element asc, trial element asc) order — the
-// accumulation order of _row_job/_col_job/dense_leaf (hmatrix.py:625-699).
-template <typename T, bool C, int OP, bool HELM, int NT, int NS>
-__device__ __forceinline__ typename Num<T, C>::V entry(const Prob<T> &P, int di, int dj,
-                                                        unsigned long long *nsing) {
-  using N = Num<T, C>;
-  if (NT == 1 && NS == 1) {
-    T re[1][1], im[1][1];
-    pair_block<T, OP, HELM, 1, 1>(P, di, dj, re, im, nsing);
-    return N::mk(re[0][0], im[0][0]);
-  }
-  typename N::V acc = N::zero();
-  const int t0 = NT == 1 ? di : P.tptr[di], t1 = NT == 1 ? di + 1 : P.tptr[di + 1];
-  const int s0 = NS == 1 ? dj : P.sptr[dj], s1 = NS == 1 ? dj + 1 : P.sptr[dj + 1];
-  for (int t = t0; t < t1; ++t) {
-    const int e = NT == 1 ? di : P.tel[t];
-    const int a = NT == 1 ? 0 : P.tloc[t];
-    for (int s = s0; s < s1; ++s) {
-      const int f = NS == 1 ? dj : P.sel[s];
-      const int b = NS == 1 ? 0 : P.sloc[s];
-      T re[NT][NS], im[NT][NS];
-      pair_block<T, OP, HELM, NT, NS>(P, e, f, re, im, nsing);
-      T vr = T(0), vi = T(0);
-#pragma unroll
-      for (int u = 0; u < NT; ++u)
-#pragma unroll
-        for (int v = 0; v < NS; ++v)
-          if (u == a && v == b) { vr = re[u][v]; vi = im[u][v]; }
-      typename N::V val = N::mk(vr, vi);
-      if constexpr (C) { acc.re += val.re; acc.im += val.im; }
-      else acc += val;
-    }
-  }
-  return acc;
-}
-
-// ---------------------------------------------------------------------------
-// ACA state
-// ---------------------------------------------------------------------------
-enum : int { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_FALLBACK = 2, ST_OVERFLOW = 3, ST_POOL = 4 };
-
-constexpr int kThreads = 128;
-constexpr int kWarps = kThreads / 32;
-constexpr int kE = 2;                  // entries per integration thread
-constexpr int kChunk = kThreads * kE;  // entries per integration CTA
-
-// Each accepted rank-1 term is one pool record [u (h) | v (w)]; v is stored
-// scaled (v = row / pivot, hmatrix.py:339) once the update is accepted.
-struct AcaDev {
-  const int *h, *w, *r0, *c0;
-  int *rank, *cur, *pcol, *small, *status, *exhausted;
-  double *norm2, *resid, *rn2, *piv;  // piv: pivot of the pending row (re, im)
-  long long *pend, *terms;
-  int tmax;
-  unsigned *rmask, *cmask;
-  const long long *rmask_off, *cmask_off;
-  void *pool;
-  long long pool_cap, pool_base;
-  int kmax_cfg;
-  double eps;
-  // wave lists: A (row phase), C (column phase), A2 (next wave)
-  const int *listA;
-  const longlong2 *needA, *scanA;  // (chunks, pool values) per position, inclusive scan
-  int *listC;
-  long long *needC;                // column chunks per position
-  const long long *scanC;
-  int *listA2;
-  longlong2 *needA2;
-  int *counts;                     // [0] |C|, [1] |A2|, [2] singular queue length
-  int2 *squeue;                    // (position, entry index) of touching P0 pairs
-  int squeue_cap;
-  unsigned long long *stat;        // [0] entries evaluated, [1] singular pairs
-  struct Job *jobs;                // per position of the current phase
-  int *cmap;                       // chunk -> position
-  void *coef;                      // per position: tmax residual coefficients
-};
-
-__device__ __forceinline__ bool better(double a, int ia, double b, int ib) {
-  return a > b || (a == b && ia < ib);
-}
-__device__ __forceinline__ void warp_argmax_sum(double &best, int &bidx, double &sum) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
-    if (better(ob, oi, best, bidx)) { best = ob; bidx = oi; }
-    sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  }
-}
-__device__ __forceinline__ bool bit(const unsigned *m, int i) { return (m[i >> 5] >> (i & 31)) & 1u; }
-__device__ __forceinline__ void set_bit(unsigned *m, int i) { atomicOr(m + (i >> 5), 1u << (i & 31)); }
-
-// lowest index without its bit set (padding bits preset), or -1
-__device__ int first_clear(const unsigned *m, int n) {
-  const int nw = (n + 31) >> 5;
-  for (int k = 0; k < nw; ++k) {
-    const unsigned v = ~m[k];
-    if (v) {
-      const int i = (k << 5) + __ffs(v) - 1;
-      return i < n ? i : -1;
-    }
-  }
-  return -1;
-}
-
-__device__ __forceinline__ int upper_pos(const long long *scan, int n, long long x) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (scan[mid] > x) hi = mid;
-    else lo = mid + 1;
-  }
-  return lo;
-}
-__device__ __forceinline__ int upper_pos2(const longlong2 *scan, int n, long long x) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (scan[mid].x > x) hi = mid;
-    else lo = mid + 1;
-  }
-  return lo;
-}
-
-__device__ __forceinline__ long long row_slot(const AcaDev &S, int pos, int b) {
-  const long long pe = S.pend[b];
-  return pe >= 0 ? pe : S.pool_base + S.scanA[pos].y - S.needA[pos].y;
-}
-
-__host__ __device__ __forceinline__ long long chunks_of(int n) { return (n + kChunk - 1) / kChunk; }
-
-// regular P0 pair value with the element data of one side already loaded
-template <typename T, bool C, int OP, bool HELM>
-__device__ __forceinline__ typename Num<T, C>::V p0_value(const Prob<T> &P, const T (&x)[18],
-                                                          const T (&na)[4], int f) {
-  T y[18], nb[4], re[1][1], im[1][1];
-  load_q<T>(P.g.q, f, y);
-  load_nj<T>(P.g.nj, f, nb);
-  regular_pair<T, OP, HELM, 1, 1>(P.R, x, y, na, nb, nullptr, nullptr, re, im);
-  return Num<T, C>::mk(re[0][0], im[0][0]);
-}
-template <typename T, bool C, int OP, bool HELM>
-__device__ __forceinline__ typename Num<T, C>::V p0_value_col(const Prob<T> &P, int e,
-                                                              const T (&y)[18],
-                                                              const T (&nb)[4]) {
-  T x[18], na[4], re[1][1], im[1][1];
-  load_q<T>(P.g.q, e, x);
-  load_nj<T>(P.g.nj, e, na);
-  regular_pair<T, OP, HELM, 1, 1>(P.R, x, y, na, nb, nullptr, nullptr, re, im);
-  return Num<T, C>::mk(re[0][0], im[0][0]);
-}
-
-// ---------------------------------------------------------------------------
-// Per-wave job tables.  After the chunk scan, one thread per job packs what
-// the integration threads need (block shape, fixed element, pending pool
-// slot, first chunk) into one record, fills the chunk -> job map and gathers
-// the residual coefficients (row phase: u_l[i]; column phase: v_l[j]), so an
-// integration thread reaches its geometry through two loads.
-// ---------------------------------------------------------------------------
-struct Job {
-  int b, h, w, k;
-  int fix;        // row phase: row i; column phase: column j
-  int r0, c0;
-  int elem;       // DOF of the fixed side (test DOF of row i / trial DOF of column j)
-  long long pe;   // pending pool slot of this block
-  long long cbase;
-};
-
-template <typename V>
-__global__ void k_jobs(AcaDev S, const int *list, int n, int col_phase, const int *rperm,
-                       const int *cperm) {
-  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pos >= n) return;
-  const int b = list[pos];
-  Job J;
-  J.b = b;
-  J.h = S.h[b];
-  J.w = S.w[b];
-  J.k = S.rank[b];
-  J.r0 = S.r0[b];
-  J.c0 = S.c0[b];
-  long long c1;
-  if (!col_phase) {
-    J.fix = S.cur[b];
-    J.pe = row_slot(S, pos, b);
-    J.elem = rperm[J.r0 + J.fix];
-    J.cbase = pos ? S.scanA[pos - 1].x : 0;
-    c1 = S.scanA[pos].x;
-  } else {
-    J.fix = S.pcol[b];
-    J.pe = S.pend[b];
-    J.elem = cperm[J.c0 + J.fix];
-    J.cbase = pos ? S.scanC[pos - 1] : 0;
-    c1 = S.scanC[pos];
-  }
-  for (long long ch = J.cbase; ch < c1; ++ch) S.cmap[ch] = pos;
-  const V *pool = static_cast<const V *>(S.pool);
-  V *coef = static_cast<V *>(S.coef) + (long long)pos * S.tmax;
-  const long long *tl = S.terms + (long long)b * S.tmax;
-  for (int l = 0; l < J.k; ++l)
-    coef[l] = col_phase ? pool[tl[l] + J.h + J.fix] : pool[tl[l] + J.fix];
-  S.jobs[pos] = J;
-}
-
-// ---------------------------------------------------------------------------
-// K3a/K3b: ACA row / column integration.  One CTA = one chunk of kChunk
-// entries of one job; each thread evaluates kE entries (integral, residual
-// update with the gathered coefficients, store).  No barriers.
-//   row:    val(c) = A(i, c) - sum_l u_l[i] v_l[c]   (hmatrix.py:323-327)
-//   column: val(r) = A(r, j) - sum_l v_l[j] u_l[r]   (hmatrix.py:340-342)
-// ---------------------------------------------------------------------------
-template <typename T, bool C, int OP, bool HELM, int NT, int NS, bool COL>
-__global__ void __launch_bounds__(kThreads) k_int(Prob<T> P, AcaDev S) {
-  using N = Num<T, C>;
-  using V = typename N::V;
-  const int pos = S.cmap[blockIdx.x];
-  const Job J = S.jobs[pos];
-  const int base = (int)(blockIdx.x - J.cbase) * kChunk;
-  const int n = COL ? J.h : J.w;
-  if (base + (int)threadIdx.x >= n) return;
-  V *pool = static_cast<V *>(S.pool);
-  const V *coef = static_cast<const V *>(S.coef) + (long long)pos * S.tmax;
-  const long long *tl = S.terms + (long long)J.b * S.tmax;
-  const int vofs = COL ? 0 : J.h;  // residual factor read at [t + vofs + idx]
-  V *dst = pool + J.pe + vofs;
-  T x[18], nx[4];
-  if constexpr (NT == 1 && NS == 1) {
-    load_q<T>(P.g.q, J.elem, x);
-    load_nj<T>(P.g.nj, J.elem, nx);
-  }
-  const int4 efix = P.elem[J.elem];
-#pragma unroll 1
-  for (int e = 0; e < kE; ++e) {
-    const int idx = base + e * kThreads + threadIdx.x;
-    if (idx >= n) break;
-    const int dof = COL ? P.rperm[J.r0 + idx] : P.cperm[J.c0 + idx];
-    V val;
-    if constexpr (NT == 1 && NS == 1) {
-      if (touching(efix, P.elem[dof])) {
-        const int q = atomicAdd(S.counts + 2, 1);
-        if (q < S.squeue_cap) S.squeue[q] = make_int2(pos, idx);
-        continue;
-      }
-      if (COL) val = p0_value_col<T, C, OP, HELM>(P, dof, x, nx);
-      else val = p0_value<T, C, OP, HELM>(P, x, nx, dof);
-    } else {
-      val = COL ? entry<T, C, OP, HELM, NT, NS>(P, dof, J.elem, S.stat + 1)
-                : entry<T, C, OP, HELM, NT, NS>(P, J.elem, dof, S.stat + 1);
-    }
-    const int ro = COL ? 0 : J.h;  // where the other factor of term l lives
-    for (int l = 0; l < J.k; ++l) val = N::fms(val, coef[l], pool[tl[l] + ro + idx]);
-    dst[idx] = val;
-  }
-}
-
-// touching P0 pairs queued by the integration kernels: warp per pair
-// (Sauter-Schwab in float64, kernels.py:249-290), then the same residual.
-template <typename T, bool C, int OP, bool HELM>
-__global__ void __launch_bounds__(kThreads) k_int_singular(Prob<T> P, AcaDev S, int col_phase) {
-  using N = Num<T, C>;
-  using V = typename N::V;
-  const int lane = threadIdx.x & 31;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  const int n = min(S.counts[2], S.squeue_cap);
-  V *pool = static_cast<V *>(S.pool);
-  for (int q = warp; q < n; q += nw) {
-    const int2 it = S.squeue[q];
-    const Job J = S.jobs[it.x];
-    const int idx = it.y;
-    const int row = col_phase ? idx : J.fix, col = col_phase ? J.fix : idx;
-    const int e = P.rperm[J.r0 + row], f = P.cperm[J.c0 + col];
-    double re[1][1], im[1][1];
-    singular_local<OP, HELM, 1, 1, 32>(P.G64, e, f, re, im);
-    if (lane == 0) {
-      V val = N::mk((T)re[0][0], (T)im[0][0]);
-      const V *coef = static_cast<const V *>(S.coef) + (long long)it.x * S.tmax;
-      const long long *tl = S.terms + (long long)J.b * S.tmax;
-      const int ro = col_phase ? 0 : J.h;
-      for (int l = 0; l < J.k; ++l) val = N::fms(val, coef[l], pool[tl[l] + ro + idx]);
-      pool[J.pe + (col_phase ? 0 : J.h) + idx] = val;
-      atomicAdd(S.stat + 1, 1ull);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K3c: row finalize, warp per block: column pivot (argmax |row| over unused
-// columns, first index on ties), vanishing-row test, schedule the column job.
-// ---------------------------------------------------------------------------
-template <typename T, bool C>
-__global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int nA) {
-  using N = Num<T, C>;
-  using V = typename N::V;
-  __shared__ unsigned long long s_ent[kWarps];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int pos = blockIdx.x * kWarps + wid;
-  unsigned long long ent = 0;
-  if (pos < nA) {
-    const int b = S.listA[pos];
-    const int h = S.h[b], w = S.w[b], i = S.cur[b];
-    const long long pe = row_slot(S, pos, b);
-    const V *row = static_cast<const V *>(S.pool) + pe + h;
-    const unsigned *cm = S.cmask + S.cmask_off[b];
-    double best = -1.0, ss = 0.0;
-    int bidx = 0x7fffffff;
-    for (int c = lane; c < w; c += 32) {
-      const V val = row[c];
-      const double a = N::abs(val);
-      ss += N::nrm(val);
-      if (!bit(cm, c) && a > best) { best = a; bidx = c; }
-    }
-    warp_argmax_sum(best, bidx, ss);
-    if (lane == 0) {
-      ent = (unsigned long long)w;
-      S.pend[b] = pe;
-      if (best <= 0.0) {
-        // residual row vanished: retire it to Z (hmatrix.py:334-338)
-        unsigned *rm = S.rmask + S.rmask_off[b];
-        set_bit(rm, i);
-        const int next = first_clear(rm, h);
-        if (next < 0) {
-          S.status[b] = ST_CONVERGED;
-          S.exhausted[b] = 1;
-        } else {
-          S.cur[b] = next;
-          const int q = atomicAdd(S.counts + 1, 1);
-          S.listA2[q] = b;
-          S.needA2[q] = make_longlong2(chunks_of(w), 0);
-        }
-      } else {
-        const V pv = row[bidx];
-        S.pcol[b] = bidx;
-        if constexpr (C) { S.piv[2 * b] = pv.re; S.piv[2 * b + 1] = pv.im; }
-        else { S.piv[2 * b] = pv; S.piv[2 * b + 1] = 0.0; }
-        S.rn2[b] = ss;
-        const int q = atomicAdd(S.counts, 1);
-        S.listC[q] = b;
-        S.needC[q] = chunks_of(h);
-      }
-    }
-  }
-  if (lane == 0) s_ent[wid] = ent;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int k = 0; k < kWarps; ++k) t += s_ent[k];
-    if (t) atomicAdd(S.stat, t);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K3d: column finalize, warp per block: |u||v| stopping test (two small
-// updates in a row stop, hmatrix.py:343-357), Frobenius update with the
-// cross terms (359-362), v = row / pivot, next row pivot argmax |u|.
-// ---------------------------------------------------------------------------
-template <typename T, bool C>
-__global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int nC) {
-  using N = Num<T, C>;
-  using V = typename N::V;
-  __shared__ unsigned long long s_ent[kWarps];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int pos = blockIdx.x * kWarps + wid;
-  unsigned long long ent = 0;
-  if (pos < nC) {
-    const int b = S.listC[pos];
-    const int h = S.h[b], w = S.w[b], i = S.cur[b], j = S.pcol[b], k = S.rank[b];
-    const long long pe = S.pend[b];
-    V *pool = static_cast<V *>(S.pool);
-    V *col = pool + pe;
-    V *row = pool + pe + h;
-    unsigned *rm = S.rmask + S.rmask_off[b];
-    double best = -1.0, ss = 0.0;
-    int bidx = 0x7fffffff;
-    for (int r = lane; r < h; r += 32) {
-      const V val = col[r];
-      const double a = N::abs(val);
-      ss += N::nrm(val);
-      if (r != i && !bit(rm, r) && a > best) { best = a; bidx = r; }
-    }
-    warp_argmax_sum(best, bidx, ss);
-    const int next = best >= 0.0 ? bidx : -1;
-    const double pr = S.piv[2 * b], pim = S.piv[2 * b + 1];
-    const double nu = sqrt(ss);
-    const double nv = sqrt(S.rn2[b]) / hypot(pr, pim);
-    const double upd = nu * nv;
-    const double n2 = S.norm2[b];
-    const int kmax_b = min(S.kmax_cfg, min(h, w));
-    ent = (unsigned long long)h;
-    if (n2 > 0.0 && upd <= S.eps * sqrt(n2)) {
-      if (lane == 0) {
-        S.resid[b] = upd / sqrt(n2);
-        const int sm = S.small[b] + 1;
-        S.small[b] = sm;
-        if (sm >= 2) {
-          S.status[b] = ST_CONVERGED;
-        } else {
-          set_bit(rm, i);
-          if (next < 0) {
-            S.status[b] = ST_CONVERGED;
-            S.exhausted[b] = 1;
-          } else {
-            S.cur[b] = next;
-            const int q = atomicAdd(S.counts + 1, 1);
-            S.listA2[q] = b;
-            S.needA2[q] = make_longlong2(chunks_of(w), 0);  // reuse the pending slot
-          }
-        }
-      }
-    } else {
-      // accept: v = row / pivot in place, then the cross terms
-      V pv;
-      if constexpr (C) pv = V{(T)pr, (T)pim};
-      else pv = (T)pr;
-      for (int c = lane; c < w; c += 32) row[c] = N::div(row[c], pv);
-      __syncwarp();
-      double cross = 0.0;
-      const long long *tl = S.terms + (long long)b * S.tmax;
-      for (int l = 0; l < k; ++l) {
-        const V *ul = pool + tl[l];
-        const V *vl = ul + h;
-        double ur = 0, ui = 0, vr = 0, vi = 0;
-        for (int r = lane; r < h; r += 32) N::cdot(ur, ui, ul[r], col[r]);
-        for (int c = lane; c < w; c += 32) N::cdot(vr, vi, vl[c], row[c]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          ur += __shfl_xor_sync(0xffffffffu, ur, o);
-          ui += __shfl_xor_sync(0xffffffffu, ui, o);
-          vr += __shfl_xor_sync(0xffffffffu, vr, o);
-          vi += __shfl_xor_sync(0xffffffffu, vi, o);
-        }
-        cross += ur * vr - ui * vi;  // Re(vdot(u_l, u) * vdot(v_l, v))
-      }
-      if (lane == 0) {
-        const double n2n = n2 + 2.0 * cross + upd * upd;
-        S.norm2[b] = n2n;
-        S.small[b] = 0;
-        S.terms[(long long)b * S.tmax + k] = pe;
-        S.pend[b] = -1;
-        S.rank[b] = k + 1;
-        set_bit(rm, i);
-        set_bit(S.cmask + S.cmask_off[b], j);
-        if (n2n > 0.0) {
-          S.resid[b] = upd / sqrt(n2n);
-          if (upd <= S.eps * sqrt(n2n)) S.small[b] = 1;
-        }
-        S.cur[b] = next;
-        // loop head of the next iteration (hmatrix.py:318-322)
-        if (k + 1 >= kmax_b) {
-          S.status[b] = ST_FALLBACK;
-        } else if (k + 1 >= S.tmax) {
-          S.status[b] = ST_OVERFLOW;
-        } else if (next < 0) {
-          S.status[b] = ST_CONVERGED;
-          S.exhausted[b] = 1;
-        } else {
-          const int q = atomicAdd(S.counts + 1, 1);
-          S.listA2[q] = b;
-          S.needA2[q] = make_longlong2(chunks_of(w), (long long)h + w);
-        }
-      }
-    }
-  }
-  if (lane == 0) s_ent[wid] = ent;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int k = 0; k < kWarps; ++k) t += s_ent[k];
-    if (t) atomicAdd(S.stat, t);
-  }
-}
-
-// initial state; the wave-0 list is the size-sorted block order
-__global__ void k_aca_init(AcaDev S, int n, const int *order, int *listA, longlong2 *needA) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= n) return;
-  const int b = order[q];
-  const int h = S.h[b], w = S.w[b];
-  listA[q] = b;
-  needA[q] = make_longlong2(chunks_of(w), (long long)h + w);
-  S.rank[b] = 0;
-  S.cur[b] = 0;
-  S.small[b] = 0;
-  S.status[b] = ST_ACTIVE;
-  S.exhausted[b] = 0;
-  S.norm2[b] = 0.0;
-  S.resid[b] = INFINITY;
-  S.pend[b] = -1;
-  unsigned *rm = S.rmask + S.rmask_off[b];
-  for (int k = 0; k < (h + 31) / 32; ++k) {
-    const int valid = min(32, h - k * 32);
-    rm[k] = valid == 32 ? 0u : ~((1u << valid) - 1u);
-  }
-  unsigned *cm = S.cmask + S.cmask_off[b];
-  for (int k = 0; k < (w + 31) / 32; ++k) cm[k] = 0u;
-}
-
-__global__ void k_zero_ll2(longlong2 *p, int n) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < n) p[q] = make_longlong2(0, 0);
-}
-__global__ void k_zero_ll(long long *p, int n) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < n) p[q] = 0;
-}
-
-struct SumLL2 {
-  __device__ __forceinline__ longlong2 operator()(const longlong2 &a, const longlong2 &b) const {
-    return make_longlong2(a.x + b.x, a.y + b.y);
-  }
-};
-
-// ---------------------------------------------------------------------------
 // K4: dense entries (near-field leaves and ACA fallback blocks).
 // tiles: (slot, first entry); slot -> (r0, c0, h, w, offset)
 // P0 touching entries are queued for the warp-per-pair singular kernel.
 // ---------------------------------------------------------------------------
-struct DenseDev {
-  const int *tile_slot;
-  const int *tile_start;
-  const int *r0, *c0, *h, *w;
-  const long long *off;
-  void *out;
-  int *sing_slot;           // queued P0 touching entries
-  long long *sing_pos;
-  unsigned long long *sing_count;
-  unsigned long long *stat;
-};
+
 
 template <typename T, bool C, int OP, bool HELM, int NT, int NS>
 __global__ void __launch_bounds__(kThreads) k_dense(Prob<T> P, DenseDev D) {
@@ -713,16 +107,16 @@ __global__ void k_expand(const int *slots, int n, AcaDev S, const long long *off
   for (long long idx = threadIdx.x; idx < (long long)h * w; idx += blockDim.x) {
     const int i = (int)(idx / w), c = (int)(idx % w);
     V acc = N::zero();
-    for (int l = 0; l < k; ++l) {
+    for (int l = 0; l < k; ++l) {  // record [u | r | p], v = r / p
       const V *t = pool + S.terms[(long long)b * S.tmax + l];
-      acc = N::fma_acc(acc, t[i], t[h + c]);
+      acc = N::fma_acc(acc, t[i], N::div(t[h + c], t[h + w]));
     }
     o[idx] = acc;
   }
 }
 
 // pack the factors of low-rank blocks [first, last) into U/V staging
-template <typename V>
+template <typename Tr, bool Cc, typename V = typename Num<Tr, Cc>::V>
 __global__ void k_pack_factors(const int *slots, int n, AcaDev S, const long long *uoff,
                                const long long *voff, long long ubase, long long vbase, V *u,
                                V *v) {
@@ -736,16 +130,18 @@ __global__ void k_pack_factors(const int *slots, int n, AcaDev S, const long lon
     for (int r = threadIdx.x; r < h; r += blockDim.x)
       u[uoff[q] - ubase + (long long)l * h + r] = t[r];
     for (int c = threadIdx.x; c < w; c += blockDim.x)
-      v[voff[q] - vbase + (long long)l * w + c] = t[h + c];
+      v[voff[q] - vbase + (long long)l * w + c] = Num<Tr, Cc>::div(t[h + c], t[h + w]);
   }
 }
 
 }  // namespace hb
 
+
 using namespace hb;
 
 // ---------------------------------------------------------------------------
-// host side: setup (partition upload, state allocation) and execute (waves)
+// host side: setup (partition upload, index structures) and execute (one
+// complete assembly: record gather, near-field leaves, ACA waves, payloads)
 // ---------------------------------------------------------------------------
 struct hbem_hmat {
   hbem_ctx *ctx = nullptr;
@@ -754,6 +150,7 @@ struct hbem_hmat {
   bool complex_ = false;
   size_t vbytes = 8;
   int nt = 1, ns = 1;
+  bool p0 = false;  // both spaces P0: register-resident record kernels
   // per leaf results (host)
   std::vector<int32_t> kind, rank, flags;
   std::vector<int64_t> off_u, off_v, off_dense;
@@ -762,16 +159,24 @@ struct hbem_hmat {
   const int *rperm = nullptr, *cperm = nullptr;
   const int *tptr = nullptr, *tel = nullptr, *sptr = nullptr, *sel = nullptr;
   const signed char *tloc = nullptr, *sloc = nullptr;
+  // tree-ordered element records (P0)
+  void *trec = nullptr, *srec = nullptr;
+  int n_rows = 0, n_cols = 0;
+  bool same_tree = false;
   // admissible blocks
   int na = 0;
   std::vector<int> adm_leaf, ah, aw, ar0, ac0;
-  int *d_order = nullptr, *listA = nullptr, *listA2 = nullptr;
-  longlong2 *needA = nullptr, *needA2 = nullptr, *scanA = nullptr;
-  long long *scanC = nullptr;
+  int *row_order = nullptr, *col_order = nullptr;
+  int *listA = nullptr, *listC = nullptr, *d_cnt = nullptr, *sel_tmp = nullptr;
   void *cub_tmp = nullptr;
   size_t cub_bytes = 0;
+  double *partA = nullptr, *partC = nullptr;
+  size_t partA_cap = 0, partC_cap = 0;  // doubles
+  long long items_cap = 0;
   AcaDev S{};
   void *pool = nullptr;
+  // pinned mailbox for the per-phase host reads
+  struct Mail { Need tot; int n; int pad; } *mail = nullptr;
   // near-field leaves
   int nd = 0;
   std::vector<int> den_leaf;
@@ -786,7 +191,8 @@ struct hbem_hmat {
   long long dense_entries = 0, u_entries = 0, v_entries = 0;
   std::vector<int> lowrank_slots;
   std::vector<int64_t> lr_uoff, lr_voff;
-  cudaStream_t side = nullptr;
+  cudaStream_t side = nullptr;  // near-field leaves, lowest priority
+  cudaStream_t hi = nullptr;    // ACA waves, highest priority
   cudaEvent_t side_done = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<void *> dev_allocs;
@@ -798,7 +204,11 @@ struct hbem_hmat {
     cudaFree(pool);
     cudaFree(dense_nf);
     cudaFree(dense_adm);
+    cudaFree(partA);
+    cudaFree(partC);
+    if (mail) cudaFreeHost(mail);
     if (side) cudaStreamDestroy(side);
+    if (hi) cudaStreamDestroy(hi);
     if (side_done) cudaEventDestroy(side_done);
     for (auto e : ev)
       if (e) cudaEventDestroy(e);
@@ -828,6 +238,23 @@ template <typename X> int dalloc(hbem_hmat *H, X **p, size_t n) {
 template <typename X> int upload(hbem_hmat *H, X **p, const std::vector<X> &v) {
   HB_CHECK(dalloc(H, p, v.size()));
   if (!v.empty()) HB_CUDA(cudaMemcpy(*p, v.data(), v.size() * sizeof(X), cudaMemcpyHostToDevice));
+  return HBEM_OK;
+}
+
+// grow-only device scratch (stream must be idle)
+int ensure(double **p, size_t *cap, size_t need) {
+  if (need <= *cap) return HBEM_OK;
+  cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  const size_t n = std::max(need + need / 4, (size_t)1 << 16);
+  cudaError_t e = cudaMalloc(p, n * sizeof(double));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(HBEM_ERR_CAPACITY, "device allocation of %zu partial-record bytes failed: %s",
+                     n * sizeof(double), cudaGetErrorString(e));
+  }
+  *cap = n;
   return HBEM_OK;
 }
 
@@ -866,6 +293,8 @@ template <typename T> Prob<T> make_prob(const hbem_hmat *H) {
   P.cperm = H->cperm;
   P.tptr = H->tptr; P.tel = H->tel; P.tloc = H->tloc;
   P.sptr = H->sptr; P.sel = H->sel; P.sloc = H->sloc;
+  P.trec = static_cast<const T *>(H->trec);
+  P.srec = static_cast<const T *>(H->srec);
   return P;
 }
 
@@ -876,15 +305,36 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   const int nt = ctx->nt, ns = ctx->ns;
   H->nt = nt;
   H->ns = ns;
+  H->p0 = nt == 1 && ns == 1;
+  H->n_rows = (int)d->n_rows;
+  H->n_cols = (int)d->n_cols;
   {
     std::vector<int> rp(d->n_rows), cp(d->n_cols);
     for (int64_t i = 0; i < d->n_rows; ++i) rp[i] = (int)d->row_perm[i];
     for (int64_t i = 0; i < d->n_cols; ++i) cp[i] = (int)d->col_perm[i];
     int *a, *b;
     HB_CHECK(upload(H, &a, rp));
-    HB_CHECK(upload(H, &b, cp));
+    H->same_tree = rp == cp;
+    if (H->same_tree) {
+      b = a;
+    } else {
+      HB_CHECK(upload(H, &b, cp));
+    }
     H->rperm = a;
     H->cperm = b;
+  }
+  if (H->p0) {
+    const size_t rb = (size_t)ctx->real_bytes();
+    const size_t L = ctx->precision == HBEM_DOUBLE ? RecLen<double>::value : RecLen<float>::value;
+    char *t = nullptr, *s = nullptr;
+    HB_CHECK(dalloc(H, &t, (size_t)H->n_rows * L * rb));
+    if (H->same_tree) {
+      s = t;
+    } else {
+      HB_CHECK(dalloc(H, &s, (size_t)H->n_cols * L * rb));
+    }
+    H->trec = t;
+    H->srec = s;
   }
   if (nt == 3) {
     Incidence I = incidence(d->test_dofmap, m, 3, d->n_rows);
@@ -922,17 +372,22 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   const int na = (int)H->adm_leaf.size();
   H->na = na;
   H->ah.resize(na); H->aw.resize(na); H->ar0.resize(na); H->ac0.resize(na);
+  std::vector<int> rnode(na), cnode(na);
   std::vector<long long> rmo(na), cmo(na);
-  long long rmw = 0, cmw = 0, sum_hw = 0;
+  long long rmw = 0, cmw = 0, sum_hw = 0, max_items = 0;
   for (int q = 0; q < na; ++q) {
     const int64_t lf = H->adm_leaf[q];
-    auto [r0, h] = rng(d->row_nodes, d->leaves[3 * lf]);
-    auto [c0, w] = rng(d->col_nodes, d->leaves[3 * lf + 1]);
+    rnode[q] = (int)d->leaves[3 * lf];
+    cnode[q] = (int)d->leaves[3 * lf + 1];
+    auto [r0, h] = rng(d->row_nodes, rnode[q]);
+    auto [c0, w] = rng(d->col_nodes, cnode[q]);
     H->ar0[q] = r0; H->ah[q] = h; H->ac0[q] = c0; H->aw[q] = w;
     rmo[q] = rmw; rmw += (h + 31) / 32;
     cmo[q] = cmw; cmw += (w + 31) / 32;
     sum_hw += h + w;
+    max_items += std::max(tiles_of(h), tiles_of(w));
   }
+  H->items_cap = std::max<long long>(max_items, 1);
   AcaDev &S = H->S;
   int tmax = d->rank_capacity > 0 ? d->rank_capacity : 64;
   S.tmax = std::min(tmax, 256);
@@ -944,16 +399,24 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
     HB_CHECK(upload(H, &p, H->aw)); S.w = p;
     HB_CHECK(upload(H, &p, H->ar0)); S.r0 = p;
     HB_CHECK(upload(H, &p, H->ac0)); S.c0 = p;
+    HB_CHECK(upload(H, &p, rnode)); S.rnode = p;
+    HB_CHECK(upload(H, &p, cnode)); S.cnode = p;
     long long *pl;
     HB_CHECK(upload(H, &pl, rmo)); S.rmask_off = pl;
     HB_CHECK(upload(H, &pl, cmo)); S.cmask_off = pl;
-    // big blocks first (load balance of the CTA-per-block waves)
+    // static phase orders: row jobs grouped by column cluster, column jobs
+    // by row cluster (ties by block index: deterministic lists)
     std::vector<int> order(na);
     std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-      return (long long)H->ah[a] * H->aw[a] > (long long)H->ah[b] * H->aw[b];
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+      return cnode[a] != cnode[b] ? cnode[a] < cnode[b] : a < b;
     });
-    HB_CHECK(upload(H, &H->d_order, order));
+    HB_CHECK(upload(H, &H->row_order, order));
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+      return rnode[a] != rnode[b] ? rnode[a] < rnode[b] : a < b;
+    });
+    HB_CHECK(upload(H, &H->col_order, order));
   }
   HB_CHECK(dalloc(H, &S.rank, na));
   HB_CHECK(dalloc(H, &S.cur, na));
@@ -966,38 +429,26 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   HB_CHECK(dalloc(H, &S.rn2, na));
   HB_CHECK(dalloc(H, &S.piv, 2 * (size_t)na));
   HB_CHECK(dalloc(H, &S.pend, na));
+  HB_CHECK(dalloc(H, &S.rowpart, na));
   HB_CHECK(dalloc(H, &S.terms, (size_t)na * S.tmax));
   HB_CHECK(dalloc(H, &S.rmask, rmw));
   HB_CHECK(dalloc(H, &S.cmask, cmw));
+  HB_CHECK(dalloc(H, &S.flagA, na));
+  HB_CHECK(dalloc(H, &S.flagC, na));
+  HB_CHECK(dalloc(H, &H->sel_tmp, (na + 3) / 4));
   HB_CHECK(dalloc(H, &H->listA, na));
-  HB_CHECK(dalloc(H, &H->listA2, na));
-  HB_CHECK(dalloc(H, &S.listC, na));
-  HB_CHECK(dalloc(H, &H->needA, na));
-  HB_CHECK(dalloc(H, &H->needA2, na));
-  HB_CHECK(dalloc(H, &H->scanA, na));
-  HB_CHECK(dalloc(H, &S.needC, na));
-  HB_CHECK(dalloc(H, &H->scanC, na));
-  HB_CHECK(dalloc(H, &S.counts, 4));
+  HB_CHECK(dalloc(H, &H->listC, na));
+  HB_CHECK(dalloc(H, &H->d_cnt, 1));
+  HB_CHECK(dalloc(H, &S.need, na));
+  HB_CHECK(dalloc(H, &S.scan, na));
+  HB_CHECK(dalloc(H, &S.jobs, na));
+  HB_CHECK(dalloc(H, &S.jt, (size_t)na * kFinRegs));
+  HB_CHECK(dalloc(H, (char **)&S.jc, (size_t)na * kFinRegs * H->vbytes));
+  HB_CHECK(dalloc(H, &S.items, H->items_cap));
   HB_CHECK(dalloc(H, &S.stat, 4));
-  {
-    // chunk map sized for the widest wave: every block's row and column
-    long long maxch = 0;
-    for (int q = 0; q < na; ++q)
-      maxch += std::max(chunks_of(H->ah[q]), chunks_of(H->aw[q]));
-    HB_CHECK(dalloc(H, &S.cmap, std::max<long long>(maxch, 1)));
-    HB_CHECK(dalloc(H, &S.jobs, na));
-    HB_CHECK(dalloc(H, (char **)&S.coef, (size_t)na * S.tmax * H->vbytes));
-  }
-  S.squeue_cap = 1 << 20;
-  HB_CHECK(dalloc(H, &S.squeue, S.squeue_cap));
-  {
-    size_t b1 = 0, b2 = 0;
-    HB_CUDA(cub::DeviceScan::InclusiveScan(nullptr, b1, H->needA, H->scanA, SumLL2(),
-                                           std::max(na, 1)));
-    HB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, b2, S.needC, H->scanC, std::max(na, 1)));
-    H->cub_bytes = std::max(b1, b2);
-    HB_CHECK(dalloc(H, (char **)&H->cub_tmp, H->cub_bytes));
-  }
+  H->cub_bytes = aca_cub_bytes(na);
+  HB_CHECK(dalloc(H, (char **)&H->cub_tmp, H->cub_bytes));
+  HB_CUDA(cudaMallocHost(&H->mail, sizeof(hbem_hmat::Mail)));
   // ---- near-field leaves --------------------------------------------------------
   const int nd = (int)H->den_leaf.size();
   H->nd = nd;
@@ -1015,22 +466,9 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   }
   H->nf_entries = tot;
   {
-    std::vector<int> tslot, tstart;
-    tslot.reserve(tot / kThreads + nd);
-    tstart.reserve(tot / kThreads + nd);
-    for (int s = 0; s < nd; ++s) {
-      const long long hw = (long long)dh[s] * dw[s];
-      for (long long t = 0; t < hw; t += kThreads) {
-        tslot.push_back(s);
-        tstart.push_back((int)t);
-      }
-    }
-    H->n_tiles = (unsigned)tslot.size();
     DenseDev &D = H->D;
     int *p;
     long long *pl;
-    HB_CHECK(upload(H, &p, tslot)); D.tile_slot = p;
-    HB_CHECK(upload(H, &p, tstart)); D.tile_start = p;
     HB_CHECK(upload(H, &p, dr0)); D.r0 = p;
     HB_CHECK(upload(H, &p, dc0)); D.c0 = p;
     HB_CHECK(upload(H, &p, dh)); D.h = p;
@@ -1038,11 +476,29 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
     HB_CHECK(upload(H, &pl, doff)); D.off = pl;
     HB_CHECK(dalloc(H, &D.sing_count, 1));
     HB_CHECK(dalloc(H, &D.stat, 2));
-    if (nt == 1 && ns == 1) {
-      // touching P0 pairs: at most ~13 per element; bound by the entry count
-      H->nf_max_sing = std::min<long long>(tot, 32 * (m + 1));
-      HB_CHECK(dalloc(H, &D.sing_slot, H->nf_max_sing));
-      HB_CHECK(dalloc(H, &D.sing_pos, H->nf_max_sing));
+    if (H->p0) {
+      // warp items (leaf, 32-column tile); touching pairs handled in-kernel
+      std::vector<int2> items;
+      for (int s = 0; s < nd; ++s)
+        for (int t = 0; t < tiles_of(dw[s]); ++t) items.push_back(make_int2(s, t));
+      int2 *pi;
+      HB_CHECK(upload(H, &pi, items));
+      D.items = pi;
+      D.n_items = (long long)items.size();
+    } else {
+      std::vector<int> tslot, tstart;
+      tslot.reserve(tot / kThreads + nd);
+      tstart.reserve(tot / kThreads + nd);
+      for (int s = 0; s < nd; ++s) {
+        const long long hw = (long long)dh[s] * dw[s];
+        for (long long t = 0; t < hw; t += kThreads) {
+          tslot.push_back(s);
+          tstart.push_back((int)t);
+        }
+      }
+      H->n_tiles = (unsigned)tslot.size();
+      HB_CHECK(upload(H, &p, tslot)); D.tile_slot = p;
+      HB_CHECK(upload(H, &p, tstart)); D.tile_start = p;
     }
   }
   const size_t vb = H->vbytes;
@@ -1052,16 +508,70 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   size_t free_b = 0, total_b = 0;
   HB_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const size_t want = (size_t)sum_hw * (size_t)std::min(S.tmax, 24) * vb;
-  const size_t reserve = ((size_t)4 << 30) + (size_t)(0.02 * (double)free_b);
+  const size_t reserve = ((size_t)6 << 30) + (size_t)(0.03 * (double)free_b);
   size_t cap_b = free_b > reserve ? free_b - reserve : 0;
   cap_b = std::min(cap_b, std::max(want, (size_t)1 << 20));
   HB_CUDA(cudaMalloc(&H->pool, std::max<size_t>(cap_b, vb)));
   S.pool = H->pool;
   S.pool_cap = (long long)(cap_b / vb);
-  HB_CUDA(cudaStreamCreateWithFlags(&H->side, cudaStreamNonBlocking));
+  {
+    // the ACA waves (latency-bound finalize phases, host reads between
+    // phases) run on a high-priority stream; the compute-bound near-field
+    // leaves on a low-priority stream fill the gaps
+    int least = 0, greatest = 0;
+    HB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    HB_CUDA(cudaStreamCreateWithPriority(&H->side, cudaStreamNonBlocking, least));
+    HB_CUDA(cudaStreamCreateWithPriority(&H->hi, cudaStreamNonBlocking, greatest));
+  }
   HB_CUDA(cudaEventCreateWithFlags(&H->side_done, cudaEventDisableTiming));
   for (auto &e : H->ev) HB_CUDA(cudaEventCreate(&e));
   return HBEM_OK;
+}
+
+// one phase of one wave: select + scan, one host read, jobs/items/integrate/finalize
+template <typename T, bool C>
+int run_phase(hbem_hmat *H, const Prob<T> &P, int col, long long &pool_top, int wave, int *n_out,
+              cudaStream_t st) {
+  hbem_ctx *ctx = H->ctx;
+  AcaDev &S = H->S;
+  PhaseArgs A{};
+  A.na = H->na;
+  A.col_phase = col;
+  A.order = col ? H->col_order : H->row_order;
+  A.cub_tmp = H->cub_tmp;
+  A.cub_bytes = H->cub_bytes;
+  A.sel_tmp = H->sel_tmp;
+  S.list = col ? H->listC : H->listA;
+  S.nlist = H->d_cnt;
+  HB_CHECK((aca_select<T, C>(P, S, A, st)));
+  HB_CUDA(cudaMemcpyAsync(&H->mail->tot, S.scan + (H->na - 1), sizeof(Need),
+                          cudaMemcpyDeviceToHost, st));
+  HB_CUDA(cudaMemcpyAsync(&H->mail->n, H->d_cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+  HB_CUDA(cudaStreamSynchronize(st));
+  const Need tot = H->mail->tot;
+  const int n = H->mail->n;
+  *n_out = n;
+  if (n == 0) return HBEM_OK;
+  if (!col) {
+    if (pool_top + tot.pool > S.pool_cap)
+      return set_error(HBEM_ERR_CAPACITY,
+                       "ACA factor pool of %lld values exhausted at wave %d (need %lld more)",
+                       (long long)S.pool_cap, wave, (long long)(pool_top + tot.pool - S.pool_cap));
+    S.pool_base = pool_top;
+    pool_top += tot.pool;
+  }
+  if (tot.items > H->items_cap)
+    return set_error(HBEM_ERR_CAPACITY, "ACA item table overflow (%lld > %lld)",
+                     (long long)tot.items, (long long)H->items_cap);
+  if (col) {
+    HB_CHECK(ensure(&H->partC, &H->partC_cap, (size_t)tot.part));
+    S.part = H->partC;
+    S.rpart = H->partA;
+  } else {
+    HB_CHECK(ensure(&H->partA, &H->partA_cap, (size_t)tot.part));
+    S.part = H->partA;
+  }
+  return aca_phase<T, C>(P, S, A, ctx->op, ctx->helm, H->nt, H->ns, n, tot.items, st);
 }
 
 template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
@@ -1076,6 +586,15 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   hbem_hmat_stats &ST = H->stats;
   const hbem_hmat_stats zero{};
   ST = zero;
+  // ---- tree-ordered element records (P0) -------------------------------------------
+  if (H->p0) {
+    HB_CHECK(build_recs<T>(P.g, ctx->elem, H->rperm, H->n_rows, static_cast<T *>(H->trec), st));
+    ++launches;
+    if (!H->same_tree) {
+      HB_CHECK(build_recs<T>(P.g, ctx->elem, H->cperm, H->n_cols, static_cast<T *>(H->srec), st));
+      ++launches;
+    }
+  }
   // ---- near-field leaves on the side stream (overlaps the ACA waves) ---------
   cudaEvent_t start_ev;
   HB_CUDA(cudaEventCreateWithFlags(&start_ev, cudaEventDisableTiming));
@@ -1086,22 +605,26 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   if (H->nd > 0) {
     HB_CUDA(cudaMemsetAsync(H->D.sing_count, 0, 8, H->side));
     HB_CUDA(cudaMemsetAsync(H->D.stat, 0, 16, H->side));
-    int rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc,
-                                                         auto NSc) -> int {
-      constexpr int OP = decltype(OPc)::value;
-      constexpr bool HH = decltype(Hc)::value != 0;
-      constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
-      k_dense<T, C, OP, HH, NT, NS><<<H->n_tiles, kThreads, 0, H->side>>>(P, H->D);
-      HB_CUDA(cudaGetLastError());
+    if (H->p0) {
+      HB_CHECK((near_p0_launch<T, C>(P, H->D, ctx->op, ctx->helm, H->side)));
       ++launches;
-      if constexpr (NT == 1 && NS == 1) {
-        k_dense_singular<T, C, OP, HH><<<148 * 16, kThreads, 0, H->side>>>(P, H->D);
-        HB_CUDA(cudaGetLastError());
-        ++launches;
-      }
-      return HBEM_OK;
-    });
-    if (rc != HBEM_OK) return rc;
+    } else {
+      int rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc,
+                                                           auto NSc) -> int {
+        constexpr int OP = decltype(OPc)::value;
+        constexpr bool HH = decltype(Hc)::value != 0;
+        constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
+        if constexpr (HH == C) {
+          k_dense<T, C, OP, HH, NT, NS><<<H->n_tiles, kThreads, 0, H->side>>>(P, H->D);
+          HB_CUDA(cudaGetLastError());
+          return HBEM_OK;
+        } else {
+          return set_error(HBEM_ERR_KERNEL, "value type does not match the equation");
+        }
+      });
+      if (rc != HBEM_OK) return rc;
+      ++launches;
+    }
   }
   HB_CUDA(cudaEventRecord(H->side_done, H->side));
   HB_CUDA(cudaEventRecord(H->ev[3], H->side));
@@ -1110,100 +633,22 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   int waves = 0;
   long long pool_top = 0;
   if (na > 0) {
-    k_aca_init<<<(na + 127) / 128, 128, 0, st>>>(S, na, H->d_order, H->listA, H->needA);
-    HB_CUDA(cudaGetLastError());
+    HB_CHECK((aca_init<T, C>(P, S, na, st)));
     ++launches;
-    int nA = na;
-    int *la = H->listA, *la2 = H->listA2;
-    longlong2 *na_ = H->needA, *na2 = H->needA2;
-    // per wave: scan(row chunks, pool) -> int_row -> singular -> fin_row ->
-    // scan(col chunks) -> int_col -> singular -> fin_col; 2 host syncs
-    while (nA > 0) {
-      S.listA = la;
-      S.needA = na_;
-      S.scanA = H->scanA;
-      S.listA2 = la2;
-      S.needA2 = na2;
-      S.scanC = H->scanC;
+    for (;;) {
       HB_CUDA(cudaEventRecord(H->ev[0], st));
-      size_t tb = H->cub_bytes;
-      HB_CUDA(cub::DeviceScan::InclusiveScan(H->cub_tmp, tb, na_, H->scanA, SumLL2(), nA, st));
-      longlong2 tot;
-      HB_CUDA(cudaMemcpyAsync(&tot, H->scanA + nA - 1, sizeof(tot), cudaMemcpyDeviceToHost, st));
-      HB_CUDA(cudaMemsetAsync(S.counts, 0, 16, st));
-      k_zero_ll<<<(nA + 255) / 256, 256, 0, st>>>(S.needC, nA);
-      k_zero_ll2<<<(nA + 255) / 256, 256, 0, st>>>(na2, nA);
-      HB_CUDA(cudaStreamSynchronize(st));
-      if (pool_top + tot.y > S.pool_cap)
-        return set_error(HBEM_ERR_CAPACITY,
-                         "ACA factor pool of %lld values exhausted at wave %d (need %lld more)",
-                         (long long)S.pool_cap, waves, (long long)(pool_top + tot.y - S.pool_cap));
-      S.pool_base = pool_top;
-      pool_top += tot.y;
-      const unsigned row_chunks = (unsigned)tot.x;
-      int rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc,
-                                                           auto NSc) -> int {
-        constexpr int OP = decltype(OPc)::value;
-        constexpr bool HH = decltype(Hc)::value != 0;
-        constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
-        k_jobs<V><<<(nA + 127) / 128, 128, 0, st>>>(S, la, nA, 0, P.rperm, P.cperm);
-        HB_CUDA(cudaGetLastError());
-        k_int<T, C, OP, HH, NT, NS, false><<<row_chunks, kThreads, 0, st>>>(P, S);
-        HB_CUDA(cudaGetLastError());
-        if constexpr (NT == 1 && NS == 1) {
-          k_int_singular<T, C, OP, HH><<<148 * 4, kThreads, 0, st>>>(P, S, 0);
-          HB_CUDA(cudaGetLastError());
-        }
-        return HBEM_OK;
-      });
-      if (rc != HBEM_OK) return rc;
-      k_fin_row<T, C><<<(nA + kWarps - 1) / kWarps, kThreads, 0, st>>>(S, nA);
-      HB_CUDA(cudaGetLastError());
-      size_t tb2 = H->cub_bytes;
-      HB_CUDA(cub::DeviceScan::InclusiveSum(H->cub_tmp, tb2, S.needC, H->scanC, nA, st));
-      int cnt[3];
-      long long col_chunks = 0;
-      HB_CUDA(cudaMemcpyAsync(cnt, S.counts, 12, cudaMemcpyDeviceToHost, st));
-      HB_CUDA(cudaMemcpyAsync(&col_chunks, H->scanC + nA - 1, 8, cudaMemcpyDeviceToHost, st));
-      HB_CUDA(cudaMemsetAsync(S.counts + 2, 0, 4, st));
-      HB_CUDA(cudaStreamSynchronize(st));
-      if (cnt[2] > S.squeue_cap)
-        return set_error(HBEM_ERR_CAPACITY, "singular queue overflow (%d touching pairs)", cnt[2]);
-      const int nC = cnt[0];
-      if (nC > 0) {
-        rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc,
-                                                         auto NSc) -> int {
-          constexpr int OP = decltype(OPc)::value;
-          constexpr bool HH = decltype(Hc)::value != 0;
-          constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
-          k_jobs<V><<<(nC + 127) / 128, 128, 0, st>>>(S, S.listC, nC, 1, P.rperm, P.cperm);
-          HB_CUDA(cudaGetLastError());
-          k_int<T, C, OP, HH, NT, NS, true><<<(unsigned)col_chunks, kThreads, 0, st>>>(P, S);
-          HB_CUDA(cudaGetLastError());
-          if constexpr (NT == 1 && NS == 1) {
-            k_int_singular<T, C, OP, HH><<<148 * 4, kThreads, 0, st>>>(P, S, 1);
-            HB_CUDA(cudaGetLastError());
-          }
-          return HBEM_OK;
-        });
-        if (rc != HBEM_OK) return rc;
-        k_fin_col<T, C><<<(nC + kWarps - 1) / kWarps, kThreads, 0, st>>>(S, nC);
-        HB_CUDA(cudaGetLastError());
-      }
-      launches += (nt == 1 && ns == 1) ? 10 : 8;
+      int nA = 0, nC = 0;
+      HB_CHECK((run_phase<T, C>(H, P, 0, pool_top, waves, &nA, st)));
+      if (nA == 0) break;
+      HB_CHECK((run_phase<T, C>(H, P, 1, pool_top, waves, &nC, st)));
+      launches += nC > 0 ? 10 : 7;
       HB_CUDA(cudaEventRecord(H->ev[1], st));
-      HB_CUDA(cudaMemcpyAsync(cnt, S.counts, 12, cudaMemcpyDeviceToHost, st));
-      HB_CUDA(cudaStreamSynchronize(st));
-      if (cnt[2] > S.squeue_cap)
-        return set_error(HBEM_ERR_CAPACITY, "singular queue overflow (%d touching pairs)", cnt[2]);
+      HB_CUDA(cudaEventSynchronize(H->ev[1]));
       float ms = 0.f;
       HB_CUDA(cudaEventElapsedTime(&ms, H->ev[0], H->ev[1]));
       ST.aca_kernel_ms += ms;
       ST.row_jobs += nA;
       ST.col_jobs += nC;
-      nA = cnt[1];
-      std::swap(la, la2);
-      std::swap(na_, na2);
       ++waves;
     }
   }
@@ -1233,9 +678,6 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
                        "ACA rank capacity %d exceeded for block rows [%d, %d) x cols [%d, %d); "
                        "raise rank_capacity",
                        S.tmax, H->ar0[q], H->ar0[q] + h, H->ac0[q], H->ac0[q] + w);
-    if (s == ST_POOL)
-      return set_error(HBEM_ERR_CAPACITY, "ACA factor pool of %lld values exhausted",
-                       (long long)S.pool_cap);
     H->rank[lf] = rk_h[q];
     H->resid[lf] = rs_h[q];
     H->flags[lf] = (s == ST_CONVERGED ? 1 : 0) | (ex_h[q] ? 2 : 0);
@@ -1289,7 +731,7 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   }
   unsigned long long fb_sing = 0;
   if (!fb_r0.empty()) {
-    // exact rows of non-converged blocks: the dense-leaf kernels on a
+    // exact rows of non-converged blocks: the generic dense kernels on a
     // temporary tile list
     DenseDev F{};
     std::vector<int> tslot, tstart;
@@ -1326,13 +768,17 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
       constexpr int OP = decltype(OPc)::value;
       constexpr bool HH = decltype(Hc)::value != 0;
       constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
-      k_dense<T, C, OP, HH, NT, NS><<<ntl, kThreads, 0, st>>>(P, F);
-      HB_CUDA(cudaGetLastError());
-      if constexpr (NT == 1 && NS == 1) {
-        k_dense_singular<T, C, OP, HH><<<148 * 16, kThreads, 0, st>>>(P, F);
+      if constexpr (HH == C) {
+        k_dense<T, C, OP, HH, NT, NS><<<ntl, kThreads, 0, st>>>(P, F);
         HB_CUDA(cudaGetLastError());
+        if constexpr (NT == 1 && NS == 1) {
+          k_dense_singular<T, C, OP, HH><<<148 * 16, kThreads, 0, st>>>(P, F);
+          HB_CUDA(cudaGetLastError());
+        }
+        return HBEM_OK;
+      } else {
+        return set_error(HBEM_ERR_KERNEL, "value type does not match the equation");
       }
-      return HBEM_OK;
     });
     if (rc != HBEM_OK) return rc;
     launches += (nt == 1 && ns == 1) ? 2 : 1;
@@ -1373,11 +819,23 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   return HBEM_OK;
 }
 
-int execute(hbem_hmat *H, cudaStream_t st) {
+int execute(hbem_hmat *H, cudaStream_t caller) {
   hbem_ctx *ctx = H->ctx;
+  cudaEvent_t e0, e1;
+  HB_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+  HB_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+  HB_CUDA(cudaEventRecord(e0, caller));
+  HB_CUDA(cudaStreamWaitEvent(H->hi, e0, 0));
+  int rc;
   if (ctx->precision == HBEM_DOUBLE)
-    return ctx->helm ? execute_t<double, true>(H, st) : execute_t<double, false>(H, st);
-  return ctx->helm ? execute_t<float, true>(H, st) : execute_t<float, false>(H, st);
+    rc = ctx->helm ? execute_t<double, true>(H, H->hi) : execute_t<double, false>(H, H->hi);
+  else
+    rc = ctx->helm ? execute_t<float, true>(H, H->hi) : execute_t<float, false>(H, H->hi);
+  cudaEventRecord(e1, H->hi);
+  cudaStreamWaitEvent(caller, e1, 0);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return rc;
 }
 
 }  // namespace
@@ -1497,16 +955,16 @@ int hbem_hmat_copy_arenas(const hbem_hmat *hc, void *u, void *v, void *dense) {
       }
       const int cnt = (int)(q1 - q0);
       if (h->vbytes == 16)
-        k_pack_factors<Cx<double>><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0,
+        k_pack_factors<double, true><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0,
                                                  ub, vbase, (Cx<double> *)su, (Cx<double> *)sv);
       else if (h->vbytes == 8 && h->complex_)
-        k_pack_factors<Cx<float>><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
+        k_pack_factors<float, true><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
                                                 vbase, (Cx<float> *)su, (Cx<float> *)sv);
       else if (h->vbytes == 8)
-        k_pack_factors<double><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
+        k_pack_factors<double, false><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
                                              vbase, (double *)su, (double *)sv);
       else
-        k_pack_factors<float><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
+        k_pack_factors<float, false><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
                                             vbase, (float *)su, (float *)sv);
       HB_CUDA(cudaGetLastError());
       if (u)

@@ -1,0 +1,448 @@
+// Shared device-side types of the H-matrix assembler (hmat.cu host side,
+// aca_impl.cuh lock-step ACA waves, near_impl.cuh near-field leaves).
+//
+// Reference: /root/reference/pkg/src/hbem/hmatrix.py
+//   aca                 271-382   (pivoting, stopping, Frobenius update)
+//   _row_job/_col_job   625-672   (entry = sum over carrying element pairs)
+//   dense_leaf          676-699
+//   assemble_hmatrix    759-811
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hbem_internal.h"
+
+namespace hb {
+
+// ---------------------------------------------------------------------------
+// value arithmetic (real T or complex as (re, im) pairs, numpy layout)
+// ---------------------------------------------------------------------------
+template <typename T> struct Cx { T re, im; };
+
+template <typename T, bool C> struct Num;
+template <typename T, bool C> struct NumV;
+template <typename T> struct Num<T, false> {
+  using V = T;
+  static constexpr int NC = 1;
+  __device__ static V mk(T r, T) { return r; }
+  __device__ static V fms(V a, V b, V c) { return a - b * c; }
+  __device__ static double abs(V a) { return fabs((double)a); }
+  __device__ static double nrm(V a) { return (double)a * (double)a; }
+  __device__ static void cdot(double &re, double &, V a, V b) { re += (double)a * (double)b; }
+  __device__ static V div(V a, V b) { return a / b; }
+  __device__ static V zero() { return T(0); }
+  __device__ static V fma_acc(V acc, V a, V b) { return acc + a * b; }
+  __device__ static T re(V a) { return a; }
+  __device__ static T im(V) { return T(0); }
+};
+template <typename T> struct Num<T, true> {
+  using V = Cx<T>;
+  static constexpr int NC = 2;
+  __device__ static V mk(T r, T i) { return V{r, i}; }
+  __device__ static V fms(V a, V b, V c) {
+    return V{a.re - (b.re * c.re - b.im * c.im), a.im - (b.re * c.im + b.im * c.re)};
+  }
+  __device__ static double abs(V a) { return hypot((double)a.re, (double)a.im); }
+  __device__ static double nrm(V a) {
+    return (double)a.re * (double)a.re + (double)a.im * (double)a.im;
+  }
+  __device__ static void cdot(double &re, double &im, V a, V b) {  // conj(a) b
+    re += (double)a.re * (double)b.re + (double)a.im * (double)b.im;
+    im += (double)a.re * (double)b.im - (double)a.im * (double)b.re;
+  }
+  __device__ static V div(V a, V b) {
+    const T d = b.re * b.re + b.im * b.im;
+    return V{(a.re * b.re + a.im * b.im) / d, (a.im * b.re - a.re * b.im) / d};
+  }
+  __device__ static V zero() { return V{T(0), T(0)}; }
+  __device__ static V fma_acc(V acc, V a, V b) {
+    return V{acc.re + (a.re * b.re - a.im * b.im), acc.im + (a.re * b.im + a.im * b.re)};
+  }
+  __device__ static T re(V a) { return a.re; }
+  __device__ static T im(V a) { return a.im; }
+};
+
+template <typename T, bool C> using V_t = typename Num<T, C>::V;
+
+// ---------------------------------------------------------------------------
+// Tree-ordered element records (P0 spaces: DOF = element).  Record tp holds
+// the element at cluster-tree position tp, so a cluster [start, start + n)
+// is n consecutive records: warps read a varying cluster coalesced and keep
+// one element per lane in registers.  Layout (T units): qpoints 18 | nx ny
+// nz |J| | (v0, v1, v2, element id) as 4 x int32, padded to 16-byte vectors.
+// ---------------------------------------------------------------------------
+template <typename T> struct RecLen;
+template <> struct RecLen<double> { static constexpr int value = 24; };  // 192 B
+template <> struct RecLen<float> { static constexpr int value = 28; };   // 112 B
+
+template <typename T> struct ElemRec {
+  T q[18];
+  T n[4];       // nx, ny, nz, |J|
+  int4 ev;      // vertex ids, element id
+};
+
+template <typename T> __device__ __forceinline__ void load_rec(const T *recs, int64_t tp,
+                                                               ElemRec<T> &r);
+template <> __device__ __forceinline__ void load_rec<double>(const double *recs, int64_t tp,
+                                                             ElemRec<double> &r) {
+  const double2 *p = reinterpret_cast<const double2 *>(recs + tp * 24);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const double2 v = __ldg(p + i);
+    r.q[2 * i] = v.x;
+    r.q[2 * i + 1] = v.y;
+  }
+  const double2 a = __ldg(p + 9), b = __ldg(p + 10);
+  r.n[0] = a.x; r.n[1] = a.y; r.n[2] = b.x; r.n[3] = b.y;
+  r.ev = __ldg(reinterpret_cast<const int4 *>(p + 11));
+}
+template <> __device__ __forceinline__ void load_rec<float>(const float *recs, int64_t tp,
+                                                            ElemRec<float> &r) {
+  const float4 *p = reinterpret_cast<const float4 *>(recs + tp * 28);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float4 v = __ldg(p + i);
+    r.q[4 * i] = v.x; r.q[4 * i + 1] = v.y; r.q[4 * i + 2] = v.z; r.q[4 * i + 3] = v.w;
+  }
+  const float4 v4 = __ldg(p + 4);
+  r.q[16] = v4.x; r.q[17] = v4.y; r.n[0] = v4.z; r.n[1] = v4.w;
+  const float4 v5 = __ldg(p + 5);
+  r.n[2] = v5.x; r.n[3] = v5.y;
+  r.ev = __ldg(reinterpret_cast<const int4 *>(p + 6));
+}
+
+// ---------------------------------------------------------------------------
+// problem view: geometry + DOF maps
+// ---------------------------------------------------------------------------
+template <typename T> struct Prob {
+  Geo<T> g;
+  RuleTab<T> R;
+  Geo64 G64;
+  const int4 *elem;
+  const int *rperm, *cperm;  // tree position -> DOF
+  // DOF -> (element, local) incidence CSR (linear spaces)
+  const int *tptr, *tel;
+  const signed char *tloc;
+  const int *sptr, *sel;
+  const signed char *sloc;
+  // P0: tree-ordered element records (test / trial tree; may alias)
+  const T *trec, *srec;
+};
+
+// block of one element pair (any adjacency), thread-level
+template <typename T, int OP, bool HELM, int NT, int NS>
+__device__ __forceinline__ void pair_block(const Prob<T> &P, int e, int f, T (&re)[NT][NS],
+                                           T (&im)[NT][NS], unsigned long long *nsing) {
+  if (touching(P.elem[e], P.elem[f])) {
+    double dr[NT][NS], di[NT][NS];
+    singular_local<OP, HELM, NT, NS, 1>(P.G64, e, f, dr, di);
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+      for (int j = 0; j < NS; ++j) { re[i][j] = (T)dr[i][j]; im[i][j] = (T)di[i][j]; }
+    if (nsing) atomicAdd(nsing, 1ull);
+    return;
+  }
+  T x[18], y[18], na[4], nb[4];
+  load_q<T>(P.g.q, e, x);
+  load_q<T>(P.g.q, f, y);
+  load_nj<T>(P.g.nj, e, na);
+  load_nj<T>(P.g.nj, f, nb);
+  const T *ca = nullptr, *cb = nullptr;
+  if (OP == HBEM_HYPS) { ca = P.g.curl + 9 * (int64_t)e; cb = P.g.curl + 9 * (int64_t)f; }
+  regular_pair<T, OP, HELM, NT, NS>(P.R, x, y, na, nb, ca, cb, re, im);
+}
+
+// Matrix entry (test DOF di, trial DOF dj): sum over the element pairs that
+// carry both DOFs, in (test element asc, trial element asc) order — the
+// accumulation order of _row_job/_col_job/dense_leaf (hmatrix.py:625-699).
+template <typename T, bool C, int OP, bool HELM, int NT, int NS>
+__device__ __forceinline__ typename Num<T, C>::V entry(const Prob<T> &P, int di, int dj,
+                                                        unsigned long long *nsing) {
+  using N = Num<T, C>;
+  if (NT == 1 && NS == 1) {
+    T re[1][1], im[1][1];
+    pair_block<T, OP, HELM, 1, 1>(P, di, dj, re, im, nsing);
+    return N::mk(re[0][0], im[0][0]);
+  }
+  typename N::V acc = N::zero();
+  const int t0 = NT == 1 ? di : P.tptr[di], t1 = NT == 1 ? di + 1 : P.tptr[di + 1];
+  const int s0 = NS == 1 ? dj : P.sptr[dj], s1 = NS == 1 ? dj + 1 : P.sptr[dj + 1];
+  for (int t = t0; t < t1; ++t) {
+    const int e = NT == 1 ? di : P.tel[t];
+    const int a = NT == 1 ? 0 : P.tloc[t];
+    for (int s = s0; s < s1; ++s) {
+      const int f = NS == 1 ? dj : P.sel[s];
+      const int b = NS == 1 ? 0 : P.sloc[s];
+      T re[NT][NS], im[NT][NS];
+      pair_block<T, OP, HELM, NT, NS>(P, e, f, re, im, nsing);
+      T vr = T(0), vi = T(0);
+#pragma unroll
+      for (int u = 0; u < NT; ++u)
+#pragma unroll
+        for (int v = 0; v < NS; ++v)
+          if (u == a && v == b) { vr = re[u][v]; vi = im[u][v]; }
+      typename N::V val = N::mk(vr, vi);
+      if constexpr (C) { acc.re += val.re; acc.im += val.im; }
+      else acc += val;
+    }
+  }
+  return acc;
+}
+
+// regular P0 pair from two element records (test x, trial y)
+template <typename T, bool C, int OP, bool HELM>
+__device__ __forceinline__ typename Num<T, C>::V p0_regular(const RuleTab<T> &R,
+                                                             const T (&x)[18], const T (&na)[4],
+                                                             const T (&y)[18], const T (&nb)[4]) {
+  T re[1][1], im[1][1];
+  regular_pair<T, OP, HELM, 1, 1>(R, x, y, na, nb, nullptr, nullptr, re, im);
+  return Num<T, C>::mk(re[0][0], im[0][0]);
+}
+
+// Point kernel of kernel_planes (kernels.py:129-158) for d = x - y:
+// SLP 1/r, DLP <d, n_y>/r^3, ADLP -<d, n_x>/r^3, Helmholtz factors e^{ikr}
+// (SLP) and (cos kr + kr sin kr, sin kr - kr cos kr) (DLP/ADLP); 1/(4 pi)
+// is applied by the caller.  nt / nf: normal of the test / trial element.
+template <typename T, int OP, bool HELM>
+__device__ __forceinline__ void point_kernel(const RuleTab<T> &R, T d0, T d1, T d2,
+                                             const T *ntest, const T *ntrial, T &gr, T &gi) {
+  const T r2 = d0 * d0 + d1 * d1 + d2 * d2;
+  const T ri = rsqrt_t<T>(r2);
+  gi = T(0);
+  if (OP == HBEM_SLP) {
+    if (!HELM) {
+      gr = ri;
+    } else {
+      const T kr = R.k * (r2 * ri);
+      T s, c;
+      sincos_t<T>(kr, &s, &c);
+      gr = ri * c;
+      gi = ri * s;
+    }
+  } else {
+    const T dot = OP == HBEM_DLP ? d0 * ntrial[0] + d1 * ntrial[1] + d2 * ntrial[2]
+                                 : -(d0 * ntest[0] + d1 * ntest[1] + d2 * ntest[2]);
+    const T amp = dot * (ri * ri * ri);
+    if (!HELM) {
+      gr = amp;
+    } else {
+      const T kr = R.k * (r2 * ri);
+      T s, c;
+      sincos_t<T>(kr, &s, &c);
+      gr = amp * (c + kr * s);
+      gi = amp * (s - kr * c);
+    }
+  }
+}
+
+// Regular P0 pairs of NJ fixed elements (points read from shared memory in
+// the inner loop, broadcast to the warp) against the lane's element in
+// registers (outer loop).  The NJ pairs are independent dependency chains
+// that share the lane's points, which doubles the instruction-level
+// parallelism at the cost of a few accumulators.  FIXED_TEST: the fixed
+// elements are test elements x (row jobs, near-field rows); otherwise trial
+// elements y (column jobs).  The double sum runs lane-side outer.
+template <typename T, bool C, int OP, bool HELM, bool FIXED_TEST, int NJ>
+__device__ __forceinline__ void p0_pairs_fx(const RuleTab<T> &R, const ElemRec<T> *const (&F)[NJ],
+                                            const T (&y)[18], const T (&nl)[4],
+                                            typename Num<T, C>::V (&out)[NJ]) {
+  T sr[NJ], si[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) { sr[j] = T(0); si[j] = T(0); }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const T y0 = y[3 * i], y1 = y[3 * i + 1], y2 = y[3 * i + 2];
+    T ar[NJ], ai[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) { ar[j] = T(0); ai[j] = T(0); }
+#pragma unroll(NJ == 1 ? 2 : 1)
+    for (int o = 0; o < 6; ++o) {
+      const T wo = FIXED_TEST ? R.wa[0][o] : R.wb[0][o];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const ElemRec<T> &G = *F[j];
+        const T d0 = FIXED_TEST ? G.q[3 * o] - y0 : y0 - G.q[3 * o];
+        const T d1 = FIXED_TEST ? G.q[3 * o + 1] - y1 : y1 - G.q[3 * o + 1];
+        const T d2 = FIXED_TEST ? G.q[3 * o + 2] - y2 : y2 - G.q[3 * o + 2];
+        T gr, gi;
+        point_kernel<T, OP, HELM>(R, d0, d1, d2, FIXED_TEST ? G.n : nl, FIXED_TEST ? nl : G.n,
+                                  gr, gi);
+        ar[j] += wo * gr;
+        if (HELM) ai[j] += wo * gi;
+      }
+    }
+    const T wi = FIXED_TEST ? R.wb[0][i] : R.wa[0][i];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      sr[j] += wi * ar[j];
+      if (HELM) si[j] += wi * ai[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const T scale = (F[j]->n[3] * nl[3]) * T(kInv4Pi);
+    out[j] = Num<T, C>::mk(scale * sr[j], HELM ? scale * si[j] : T(0));
+  }
+}
+
+// warp-cooperative Sauter-Schwab value of the touching pair (e test, f
+// trial) in float64 (local_matrix, kernels.py:330-347), kept out of line so
+// its registers do not bound the occupancy of the regular path
+template <int OP, bool HELM>
+__device__ __noinline__ double2 singular_warp(const Geo64 G, int e, int f) {
+  double re[1][1], im[1][1];
+  singular_local<OP, HELM, 1, 1, 32>(G, e, f, re, im);
+  return make_double2(re[0][0], im[0][0]);
+}
+
+__device__ __forceinline__ bool touching4(const int4 &a, const int4 &b) {
+  return a.x == b.x || a.x == b.y || a.x == b.z || a.y == b.x || a.y == b.y || a.y == b.z ||
+         a.z == b.x || a.z == b.y || a.z == b.z;
+}
+
+// ---------------------------------------------------------------------------
+// warp helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool better(double a, int ia, double b, int ib) {
+  return a > b || (a == b && ia < ib);
+}
+__device__ __forceinline__ void warp_argmax_sum(double &best, int &bidx, double &sum) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (better(ob, oi, best, bidx)) { best = ob; bidx = oi; }
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  }
+}
+__device__ __forceinline__ bool bit(const unsigned *m, int i) { return (m[i >> 5] >> (i & 31)) & 1u; }
+__device__ __forceinline__ void set_bit(unsigned *m, int i) { atomicOr(m + (i >> 5), 1u << (i & 31)); }
+
+// lowest index without its bit set (padding bits preset), or -1
+__device__ __forceinline__ int first_clear(const unsigned *m, int n) {
+  const int nw = (n + 31) >> 5;
+  for (int k = 0; k < nw; ++k) {
+    const unsigned v = ~m[k];
+    if (v) {
+      const int i = (k << 5) + __ffs(v) - 1;
+      return i < n ? i : -1;
+    }
+  }
+  return -1;
+}
+
+// ---------------------------------------------------------------------------
+// ACA state (one entry per admissible block b)
+// ---------------------------------------------------------------------------
+enum : int { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_FALLBACK = 2, ST_OVERFLOW = 3 };
+
+constexpr int kThreads = 128;
+constexpr int kWarps = kThreads / 32;
+constexpr int kFinRegs = 8;  // terms gathered per job by k_jobs and held in registers by k_fin
+
+// One ACA job of the current phase: the next row (row phase) or pivot column
+// (column phase) of block b.  The "fixed" index is the row i / column j; the
+// "varying" side is the column / row cluster the entries run over.
+struct Job {
+  int b, key;       // block, grouping key (varying-side cluster node)
+  int fix;          // row i / column j within the block
+  int h, w, k;      // block shape, accepted rank so far
+  int nfix;         // tree position of the fixed DOF
+  int vstart, nvar; // varying cluster start (tree position) and length
+  int cur;          // column phase: the block's current row i (excluded from the next pivot)
+  long long pe;     // pool record of the pending term [u (h) | v (w)]
+  long long part;   // first partial record of this job (doubles)
+};
+
+// partial record per (job, 32-wide tile): best |val| over unmasked entries,
+// its index, sum |val|^2, then k dots (re, im for complex) with the factor
+// the residual used: row phase vdot(v_l, row), column phase vdot(u_l, col).
+__host__ __device__ __forceinline__ long long part_len(int k, int nc) { return 3 + (long long)k * nc; }
+__host__ __device__ __forceinline__ int tiles_of(int n) { return (n + 31) >> 5; }
+
+struct Need {  // per-position allocation need (pool values, partial doubles, items)
+  long long pool, part, items;
+};
+struct SumNeed {
+  __device__ __forceinline__ Need operator()(const Need &a, const Need &b) const {
+    return Need{a.pool + b.pool, a.part + b.part, a.items + b.items};
+  }
+};
+
+struct AcaDev {
+  // static per block
+  const int *h, *w, *r0, *c0, *rnode, *cnode;
+  // iteration state
+  int *rank, *cur, *pcol, *small, *status, *exhausted;
+  double *norm2, *resid, *rn2, *piv;  // piv: pivot of the pending row (re, im)
+  long long *pend, *terms;            // pending record, accepted term records (tmax per block)
+  long long *rowpart;                 // row-phase partial record 0 of the block's pending row
+  int tmax;
+  unsigned *rmask, *cmask;
+  const long long *rmask_off, *cmask_off;
+  void *pool;
+  long long pool_cap, pool_base;
+  int kmax_cfg;
+  double eps;
+  unsigned char *flagA, *flagC;  // block needs a row job next wave / a column job this wave
+  // current phase
+  const int *list;   // positions -> block (sorted by key)
+  const int *nlist;  // device count of list
+  Need *need, *scan;
+  Job *jobs;
+  int2 *items;       // (head position, tile)
+  double *part;      // dot records of the current phase (k values per job)
+  long long *jt;     // per job: record offsets of its first kFinRegs terms
+  void *jc;          // per job: their residual coefficients (u_l[i] / p_l or r_l[j] / p_l)
+  const double *rpart;  // row-phase partial records (read by the column finalize)
+  unsigned long long *stat;  // [0] entries evaluated, [1] singular pairs
+};
+
+// ---------------------------------------------------------------------------
+// dense entries (near-field leaves and ACA fallback blocks)
+// ---------------------------------------------------------------------------
+struct DenseDev {
+  const int *tile_slot;
+  const int *tile_start;
+  const int *r0, *c0, *h, *w;
+  const long long *off;
+  void *out;
+  int *sing_slot;           // queued P0 touching entries
+  long long *sing_pos;
+  unsigned long long *sing_count;
+  unsigned long long *stat;
+  // P0 warp items: (slot, column tile)
+  const int2 *items;
+  long long n_items;
+};
+
+// ---------------------------------------------------------------------------
+// launchers (aca_f64.cu / aca_f32.cu, near_f64.cu / near_f32.cu)
+// ---------------------------------------------------------------------------
+struct PhaseArgs {
+  int na;             // admissible blocks
+  int col_phase;
+  const int *order;   // static block order of this phase (sorted by key)
+  void *cub_tmp;
+  size_t cub_bytes;
+  int *sel_tmp;       // na flags scratch for the compaction
+};
+
+template <typename T, bool C>
+int aca_init(const Prob<T> &P, AcaDev &S, int na, cudaStream_t st);
+// list selection + need scan (no host sync)
+template <typename T, bool C>
+int aca_select(const Prob<T> &P, AcaDev &S, const PhaseArgs &A, cudaStream_t st);
+// jobs + items + integration + finalize for a phase of n jobs and n_items items
+template <typename T, bool C>
+int aca_phase(const Prob<T> &P, AcaDev &S, const PhaseArgs &A, int op, bool helm, int nt, int ns,
+              int n, long long n_items, cudaStream_t st);
+size_t aca_cub_bytes(int na);
+
+template <typename T>
+int build_recs(const Geo<T> &g, const int4 *elem, const int *perm, int n, T *recs, cudaStream_t st);
+template <typename T, bool C>
+int near_p0_launch(const Prob<T> &P, const DenseDev &D, int op, bool helm, cudaStream_t st);
+
+}  // namespace hb

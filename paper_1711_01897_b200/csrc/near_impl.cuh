@@ -1,0 +1,121 @@
+// Near-field (inadmissible) dense leaves for P0 spaces (dense_leaf,
+// hmatrix.py:676-699) and the tree-ordered element record gather.
+//
+// One warp per (leaf, 32-column tile): lane l keeps the trial element of
+// leaf column 32 t + l in registers, test elements of 32 rows at a time are
+// staged in shared memory and broadcast; rows are stored coalesced.
+// Touching pairs (shared vertex / edge / identical) are integrated by the
+// whole warp with the Sauter-Schwab rules (kernels.py:249-347) and handed
+// back to the owning lane, so no element integral leaves the device.
+#pragma once
+#include "hmat_common.cuh"
+
+namespace hb {
+
+// record tp <- element perm[tp] (ctx geometry, element-indexed)
+template <typename T>
+__global__ void k_build_recs(Geo<T> g, const int4 *elem, const int *perm, int n, T *recs) {
+  const int tp = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tp >= n) return;
+  const int e = perm[tp];
+  constexpr int L = RecLen<T>::value;
+  T q[18], nj[4];
+  load_q<T>(g.q, e, q);
+  load_nj<T>(g.nj, e, nj);
+  T *r = recs + (int64_t)tp * L;
+#pragma unroll
+  for (int i = 0; i < 18; ++i) r[i] = q[i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) r[18 + i] = nj[i];
+  const int4 v = elem[e];
+  int4 *ev = reinterpret_cast<int4 *>(r + L - 16 / sizeof(T));
+  *ev = make_int4(v.x, v.y, v.z, e);
+}
+
+template <typename T, bool C, int OP, bool HELM>
+__global__ void __launch_bounds__(kThreads, 4) k_near_p0(Prob<T> P, DenseDev D) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  constexpr unsigned kAll = 0xffffffffu;
+  __shared__ ElemRec<T> sr[kWarps][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long item = (long long)blockIdx.x * kWarps + wid;
+  if (item >= D.n_items) return;
+  const int2 it = D.items[item];
+  const int s = it.x, t = it.y;
+  const int h = D.h[s], w = D.w[s], r0 = D.r0[s], c0 = D.c0[s];
+  const int c = t * 32 + lane;
+  const bool valid = c < w;
+  ElemRec<T> my;
+  load_rec<T>(P.srec, c0 + (valid ? c : w - 1), my);
+  V *out = static_cast<V *>(D.out) + D.off[s];
+  unsigned long long nsing = 0;
+  for (int seg = 0; seg < h; seg += 32) {
+    const int nseg = min(32, h - seg);
+    if (lane < nseg) {
+      ElemRec<T> r;
+      load_rec<T>(P.trec, r0 + seg + lane, r);
+      sr[wid][lane] = r;
+    }
+    __syncwarp();
+    for (int i = 0; i < nseg; i += 2) {
+      const int nj = i + 1 < nseg ? 2 : 1;
+      V val[2];
+      if (nj == 2) {
+        const ElemRec<T> *const F2[2] = {&sr[wid][i], &sr[wid][i + 1]};
+        p0_pairs_fx<T, C, OP, HELM, true, 2>(P.R, F2, my.q, my.n, val);
+      } else {
+        const ElemRec<T> *const F1[1] = {&sr[wid][i]};
+        V v1[1];
+        p0_pairs_fx<T, C, OP, HELM, true, 1>(P.R, F1, my.q, my.n, v1);
+        val[0] = v1[0];
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (u < nj) {
+          const int4 fev = sr[wid][i + u].ev;
+          unsigned tm = __ballot_sync(kAll, valid && touching4(fev, my.ev));
+          while (tm) {
+            const int src = __ffs(tm) - 1;
+            tm &= tm - 1;
+            const int ev = __shfl_sync(kAll, my.ev.w, src);
+            const double2 sv = singular_warp<OP, HELM>(P.G64, fev.w, ev);
+            if (lane == src) val[u] = N::mk((T)sv.x, (T)sv.y);
+            ++nsing;
+          }
+          if (valid) out[(long long)(seg + i + u) * w + c] = val[u];
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && nsing) atomicAdd(D.stat + 1, nsing);
+}
+
+template <typename T, bool C>
+int near_p0_launch(const Prob<T> &P, const DenseDev &D, int op, bool helm, cudaStream_t st) {
+  if (D.n_items <= 0) return HBEM_OK;
+  const unsigned grid = (unsigned)((D.n_items + kWarps - 1) / kWarps);
+  return dispatch_op(op, helm, 1, 1, [&](auto OPc, auto Hc, auto, auto) -> int {
+    constexpr int OP = decltype(OPc)::value;
+    constexpr bool HH = decltype(Hc)::value != 0;
+    if constexpr (HH == C && OP != HBEM_HYPS) {
+      k_near_p0<T, C, OP, HH><<<grid, kThreads, 0, st>>>(P, D);
+      HB_CUDA(cudaGetLastError());
+      return HBEM_OK;
+    } else {
+      return set_error(HBEM_ERR_KERNEL, "unsupported P0 near-field operator");
+    }
+  });
+}
+
+template <typename T>
+int build_recs(const Geo<T> &g, const int4 *elem, const int *perm, int n, T *recs,
+               cudaStream_t st) {
+  if (n <= 0) return HBEM_OK;
+  k_build_recs<T><<<(n + 127) / 128, 128, 0, st>>>(g, elem, perm, n, recs);
+  HB_CUDA(cudaGetLastError());
+  return HBEM_OK;
+}
+
+}  // namespace hb
