@@ -476,8 +476,22 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
     HB_CHECK(upload(H, &pl, doff)); D.off = pl;
     HB_CHECK(dalloc(H, &D.sing_count, 1));
     HB_CHECK(dalloc(H, &D.stat, 2));
+    if (H->p0 && nd > 0) {
+      // touching element pairs integrated once per execute into a table the
+      // near-field kernel reads (single layer: each unordered pair once)
+      SingTable tab;
+      HB_CHECK(build_sing_table(ctx->elem, (int)m, (int)ctx->nv, ctx->op == HBEM_SLP, tab,
+                                H->dev_allocs, 0));
+      D.nb_ptr = tab.nb_ptr;
+      D.nb_idx = tab.nb_idx;
+      D.spairs = tab.pairs;
+      D.n_spairs = tab.n_pairs;
+      char *st_vals = nullptr;
+      HB_CHECK(dalloc(H, &st_vals, (size_t)tab.nnz * H->vbytes));
+      D.stab = st_vals;
+    }
     if (H->p0) {
-      // warp items (leaf, 32-column tile); touching pairs handled in-kernel
+      // warp items (leaf, 32-column tile); touching pairs read from the table
       std::vector<int2> items;
       for (int s = 0; s < nd; ++s)
         for (int t = 0; t < tiles_of(dw[s]); ++t) items.push_back(make_int2(s, t));
@@ -606,8 +620,9 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
     HB_CUDA(cudaMemsetAsync(H->D.sing_count, 0, 8, H->side));
     HB_CUDA(cudaMemsetAsync(H->D.stat, 0, 16, H->side));
     if (H->p0) {
+      HB_CHECK((sing_table_launch<T, C>(P, H->D, ctx->op, ctx->helm, H->side)));
       HB_CHECK((near_p0_launch<T, C>(P, H->D, ctx->op, ctx->helm, H->side)));
-      ++launches;
+      launches += 2;
     } else {
       int rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc,
                                                            auto NSc) -> int {

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "hbem_internal.h"
 
 namespace hb {
@@ -415,7 +417,22 @@ struct DenseDev {
   // P0 warp items: (slot, column tile)
   const int2 *items;
   long long n_items;
+  // P0 singular table: element -> sorted touching elements (CSR) and the
+  // Sauter-Schwab value of every (element, neighbour) entry
+  const int *nb_ptr, *nb_idx;
+  void *stab;
+  const int4 *spairs;  // (test e, trial f, slot of (e,f), slot of (f,e) or -1)
+  long long n_spairs;
 };
+
+// P0 singular-table construction (setup) and evaluation (execute)
+struct SingTable {
+  int *nb_ptr = nullptr, *nb_idx = nullptr;
+  int4 *pairs = nullptr;
+  long long nnz = 0, n_pairs = 0;
+};
+int build_sing_table(const int4 *d_elem, int m, int nv, bool symmetric, SingTable &out,
+                     std::vector<void *> &allocs, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // launchers (aca_f64.cu / aca_f32.cu, near_f64.cu / near_f32.cu)
@@ -442,6 +459,8 @@ size_t aca_cub_bytes(int na);
 
 template <typename T>
 int build_recs(const Geo<T> &g, const int4 *elem, const int *perm, int n, T *recs, cudaStream_t st);
+template <typename T, bool C>
+int sing_table_launch(const Prob<T> &P, const DenseDev &D, int op, bool helm, cudaStream_t st);
 template <typename T, bool C>
 int near_p0_launch(const Prob<T> &P, const DenseDev &D, int op, bool helm, cudaStream_t st);
 

@@ -20,4 +20,8 @@ template int near_p0_launch<float, true>(const Prob<float> &, const DenseDev &, 
                                           cudaStream_t);
 template int build_recs<float>(const Geo<float> &, const int4 *, const int *, int, float *,
                                 cudaStream_t);
+template int sing_table_launch<float, false>(const Prob<float> &, const DenseDev &, int, bool,
+                                             cudaStream_t);
+template int sing_table_launch<float, true>(const Prob<float> &, const DenseDev &, int, bool,
+                                            cudaStream_t);
 }  // namespace hb

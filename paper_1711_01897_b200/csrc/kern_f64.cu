@@ -21,4 +21,8 @@ template int near_p0_launch<double, true>(const Prob<double> &, const DenseDev &
                                           cudaStream_t);
 template int build_recs<double>(const Geo<double> &, const int4 *, const int *, int, double *,
                                 cudaStream_t);
+template int sing_table_launch<double, false>(const Prob<double> &, const DenseDev &, int, bool,
+                                             cudaStream_t);
+template int sing_table_launch<double, true>(const Prob<double> &, const DenseDev &, int, bool,
+                                            cudaStream_t);
 }  // namespace hb

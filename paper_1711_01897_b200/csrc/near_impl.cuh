@@ -8,6 +8,8 @@
 // whole warp with the Sauter-Schwab rules (kernels.py:249-347) and handed
 // back to the owning lane, so no element integral leaves the device.
 #pragma once
+#include <algorithm>
+
 #include "hmat_common.cuh"
 
 namespace hb {
@@ -74,13 +76,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_near_p0(Prob<T> P, DenseDev D) 
       for (int u = 0; u < 2; ++u) {
         if (u < nj) {
           const int4 fev = sr[wid][i + u].ev;
-          unsigned tm = __ballot_sync(kAll, valid && touching4(fev, my.ev));
-          while (tm) {
-            const int src = __ffs(tm) - 1;
-            tm &= tm - 1;
-            const int ev = __shfl_sync(kAll, my.ev.w, src);
-            const double2 sv = singular_warp<OP, HELM>(P.G64, fev.w, ev);
-            if (lane == src) val[u] = N::mk((T)sv.x, (T)sv.y);
+          if (valid && touching4(fev, my.ev)) {
+            // Sauter-Schwab value from the singular table (computed once per
+            // touching element pair, k_sing_table)
+            const int b0 = D.nb_ptr[fev.w], b1 = D.nb_ptr[fev.w + 1];
+            int j = b0;
+            while (j < b1 && D.nb_idx[j] != my.ev.w) ++j;
+            val[u] = static_cast<const V *>(D.stab)[j];
             ++nsing;
           }
           if (valid) out[(long long)(seg + i + u) * w + c] = val[u];
@@ -89,7 +91,57 @@ __global__ void __launch_bounds__(kThreads, 4) k_near_p0(Prob<T> P, DenseDev D) 
     }
     __syncwarp();
   }
+  nsing = (unsigned long long)__reduce_add_sync(kAll, (unsigned)nsing);
   if (lane == 0 && nsing) atomicAdd(D.stat + 1, nsing);
+}
+
+
+// ---------------------------------------------------------------------------
+// Singular table (P0): one warp per touching element pair (e, f) computes
+// local_matrix(e, f) (kernels.py:330-347, canonical test>trial transpose
+// included) in float64 and stores it at the (e, f) entry of e's neighbour
+// list; for the single layer the value is symmetric bit for bit
+// (S = S^T, kernels.py:340-344), so it is also stored at (f, e) and each
+// unordered pair is integrated once.
+// ---------------------------------------------------------------------------
+template <typename T, bool C, int OP, bool HELM>
+__global__ void __launch_bounds__(kThreads) k_sing_table(Prob<T> P, DenseDev D) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  const int lane = threadIdx.x & 31;
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  V *tab = static_cast<V *>(D.stab);
+  for (long long q = warp; q < D.n_spairs; q += nw) {
+    const int4 pr = D.spairs[q];
+    double re[1][1], im[1][1];
+    singular_local<OP, HELM, 1, 1, 32>(P.G64, pr.x, pr.y, re, im);
+    if (lane == 0) {
+      const V v = N::mk((T)re[0][0], (T)im[0][0]);
+      tab[pr.z] = v;
+      if (pr.w >= 0) tab[pr.w] = v;
+    }
+  }
+}
+
+template <typename T, bool C>
+int sing_table_launch(const Prob<T> &P, const DenseDev &D, int op, bool helm, cudaStream_t st) {
+  if (D.n_spairs <= 0) return HBEM_OK;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const unsigned grid =
+      (unsigned)std::min<long long>((D.n_spairs + kWarps - 1) / kWarps, (long long)sms * 16);
+  return dispatch_op(op, helm, 1, 1, [&](auto OPc, auto Hc, auto, auto) -> int {
+    constexpr int OP = decltype(OPc)::value;
+    constexpr bool HH = decltype(Hc)::value != 0;
+    if constexpr (HH == C && OP != HBEM_HYPS) {
+      k_sing_table<T, C, OP, HH><<<grid, kThreads, 0, st>>>(P, D);
+      HB_CUDA(cudaGetLastError());
+      return HBEM_OK;
+    } else {
+      return set_error(HBEM_ERR_KERNEL, "unsupported P0 singular-table operator");
+    }
+  });
 }
 
 template <typename T, bool C>
