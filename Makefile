@@ -2,7 +2,7 @@
 NVCC    ?= nvcc
 ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
-           --expt-relaxed-constexpr -Xptxas -v
+           --expt-relaxed-constexpr -Xptxas -v $(EXTRA)
 CXXFLAGS:= -O3 -std=c++17 -fPIC -ffp-contract=off -Wall
 SRC_DIR := paper_1711_01897_b200/csrc
 BUILD   := build

@@ -47,6 +47,9 @@ UNIT = "element-pair integrals/s"
 # 36 quadrature-point pairs x (diff 3 + r^2 5 + accumulate 2) = 360 FLOP
 # (+ 36 rsqrt, not counted as FLOP)
 FLOP_PER_PAIR_LAP_SLP_P0 = 360
+# issued FP64 instructions per regular pair in k_aca_p0 (SASS: 3 DADD, DMUL + 2 DFMA,
+# MUFU.RSQ64H + 5 refinement, 1 accumulate per quadrature-point pair) + 2 epilogue
+DP_INSTR_PER_PAIR = 12 * 36 + 2
 
 
 def parse():
@@ -277,6 +280,7 @@ def run_ours(args):
         part.execute(sptr)
     barrier()
     aca_ms, nf_ms, pairs, sing, aca_entries, launches = [], [], 0, 0, 0, 0
+    int_ms, int_launches = 0.0, 0
     with ClockSampler(local) as clocks:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
@@ -291,6 +295,8 @@ def run_ours(args):
             sing += s["singular_pairs"]
             aca_entries += s["aca_entries"]
             launches += s["launches"]
+            int_ms += s["int_kernel_ms"]
+            int_launches += s["int_launches"]
         t_end.record(stream)
         barrier()
     elapsed = t_start.elapsed_time(t_end) / 1e3
@@ -307,22 +313,30 @@ def run_ours(args):
     per_step = elapsed / args.steps
     value = pairs / elapsed
 
-    # dominant kernels: the ACA row+column launches (FP64 FMA-pipe bound)
-    aca_regular = aca_entries  # P0: one pair per evaluated entry (singular ones are ~0 here)
-    aca_s = sum(aca_ms) / 1e3
-    flop_rate = FLOP_PER_PAIR_LAP_SLP_P0 * aca_regular / aca_s if aca_s > 0 else 0.0
+    # dominant kernel: k_aca_p0 (ACA row/column integration + fused residual),
+    # FP64-pipe bound; CUDA events around each launch on its stream
+    int_s = int_ms / 1e3
+    flop_rate = FLOP_PER_PAIR_LAP_SLP_P0 * aca_entries / int_s if int_s > 0 else 0.0
     peak = C.c_double(0.0)
     _lib.check(_lib.lib.hbem_probe_fma(local, _lib.PRECISIONS[args.precision], C.byref(peak)))
+    dp_issue = DP_INSTR_PER_PAIR * aca_entries / int_s if int_s > 0 else 0.0
     roofline = {"bound": "fp64" if args.precision == "double" else "fp32",
-                "kernel": "k_aca_row + k_aca_col (lock-step ACA waves)",
+                "kernel": "k_aca_p0 (ACA row/column integration, fused residual + tile statistics)",
                 "achieved": flop_rate / 1e12, "peak": peak.value / 1e12, "unit": "TFLOP/s",
                 "frac": flop_rate / peak.value if peak.value else None,
-                "peak_source": "measured live: hbem_probe_fma (DFMA chain, 2 FLOP/FMA) on this GPU",
-                "algorithmic": f"{FLOP_PER_PAIR_LAP_SLP_P0} FLOP per regular pair (SURVEY §8d)",
-                "aca_kernel_ms_per_step": float(np.mean(aca_ms)),
-                "nearfield_kernel_ms_per_step": float(np.mean(nf_ms)),
-                "aca_pairs_per_s": aca_regular / aca_s if aca_s > 0 else None,
-                "traffic": None}
+                "traffic": None,
+                "peak_source": "measured live on this GPU: hbem_probe_fma (independent DFMA "
+                               "chains, 2 FLOP per FMA); MEASURED_PEAKS.json has no FP64 figure",
+                "algorithmic": f"{FLOP_PER_PAIR_LAP_SLP_P0} FLOP per regular pair (SURVEY 8d) x "
+                               f"{aca_entries // max(args.steps, 1)} ACA entries per step",
+                "issue_frac": dp_issue / (peak.value / 2) if peak.value else None,
+                "issue_model": f"{DP_INSTR_PER_PAIR} FP64 instructions per pair (12 per "
+                               "quadrature-point pair, from cuobjdump -sass) / FP64 lane rate",
+                "launches_per_step": int_launches // max(args.steps, 1),
+                "avg_launch_ms": int_ms / max(int_launches, 1),
+                "int_kernel_ms_per_step": int_ms / max(args.steps, 1),
+                "aca_waves_ms_per_step": float(np.mean(aca_ms)),
+                "nearfield_kernel_ms_per_step": float(np.mean(nf_ms))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -347,20 +361,26 @@ def run_ours(args):
         barrier()
         t0 = time.perf_counter()
         dev2 = init_gpu_device(ictx, local)
+        t1 = time.perf_counter()
         part2 = _assemble_part(dev2, bt, ids, sp, sp, cfg, acfg, stream=sptr)
+        t2 = time.perf_counter()
         out = (np.empty(0), np.empty(0), np.empty(0))
         s2 = part2.stats
         if s2["u_entries"] == len(pinned[0]) and s2["dense_entries"] == len(pinned[2]):
             out = pinned
         part2.arenas(out=out if len(out[0]) else None)
         torch.cuda.synchronize()
-        t_e2e = time.perf_counter() - t0
+        t3 = time.perf_counter()
+        t_e2e = t3 - t0
+        split = {"context_s": t1 - t0, "setup_s": float(s2["seconds_setup"]),
+                 "assemble_s": float(s2["seconds"]), "plan_and_assemble_s": t2 - t1,
+                 "d2h_s": t3 - t2}
         if dist is not None:
             tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_e2e = float(tt.item())
         e2e = {"value": pairs / args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "seconds": t_e2e,
+               "d2h_bytes_per_step": int(d2h), "seconds": t_e2e, "split": split,
                "path": "GpuDeviceContext + assemble (hbem_ctx_create, hbem_hmat_assemble) + "
                        "hbem_hmat_copy_arenas into pinned host arenas"}
         part = part2

@@ -191,6 +191,8 @@ typedef struct hbem_hmat_stats {
   double seconds_setup;      /* one-time partition upload + allocation */
   double seconds_aca;        /* ACA waves (near-field overlapped) */
   double seconds_finalize;   /* payload classification + dense expansion */
+  double int_kernel_ms;      /* CUDA-event time of the ACA integration launches (k_aca_*) */
+  int64_t int_launches;      /* number of those launches */
 } hbem_hmat_stats;
 
 /* setup (partition upload, state allocation) + one execute */

@@ -12,7 +12,7 @@ import os
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhbem_b200.so")
+LIB_PATH = os.environ.get("HBEM_LIB") or os.path.join(_HERE, "libhbem_b200.so")
 
 HBEM_OK = 0
 _CODE_TO_EXC = {
@@ -90,7 +90,8 @@ class HmatStats(C.Structure):
         "col_jobs", "capacity_retries", "u_entries", "v_entries", "dense_entries",
         "launches", "aca_entries")] + [
         (n, C.c_double) for n in ("aca_kernel_ms", "nearfield_kernel_ms", "seconds",
-                                  "seconds_setup", "seconds_aca", "seconds_finalize")]
+                                  "seconds_setup", "seconds_aca", "seconds_finalize")] + [
+        ("int_kernel_ms", C.c_double), ("int_launches", C.c_int64)]
 
 
 # (name, restype, argtypes) of every exported symbol in include/hbem_b200.h

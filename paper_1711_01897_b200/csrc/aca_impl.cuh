@@ -336,7 +336,7 @@ __device__ __forceinline__ bool stage_job(const AcaDev &S, int p, int n, int key
 // behind the quadrature.
 // ---------------------------------------------------------------------------
 template <typename T, bool C, int OP, bool HELM, bool COL>
-__global__ void __launch_bounds__(kThreads, 4) k_aca_p0(Prob<T> P, AcaDev S, int n,
+__global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, AcaDev S, int n,
                                                         long long n_items) {
   using N = Num<T, C>;
   using V = typename N::V;
@@ -516,6 +516,7 @@ __device__ __forceinline__ void combine_tiles(const double *rec, int nt, long lo
   best = -1.0;
   bidx = 0x7fffffff;
   ss = 0.0;
+#pragma unroll 4
   for (int t = 0; t < nt; ++t) {
     const double *r = rec + t * RL;
     const double a = r[0];
@@ -525,8 +526,20 @@ __device__ __forceinline__ void combine_tiles(const double *rec, int nt, long lo
   }
 }
 
-// row finalize: column pivot (hmatrix.py:329-332) or vanishing row (334-338);
-// the dot totals over the tiles are kept in tile 0 for the column finalize
+// sum of the dots of k terms over nt tile records (fixed tile order)
+template <int NC>
+__device__ __forceinline__ void sum_dots(const double *rec, int nt, long long RL, int l,
+                                         double &sr, double &si) {
+  sr = 0.0;
+  si = 0.0;
+#pragma unroll 4
+  for (int t = 0; t < nt; ++t) {
+    sr += rec[t * RL + 3 + (long long)l * NC];
+    if (NC == 2) si += rec[t * RL + 3 + (long long)l * NC + 1];
+  }
+}
+
+// row finalize: column pivot (hmatrix.py:329-332) or vanishing row (334-338)
 template <typename T, bool C>
 __global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int n) {
   using N = Num<T, C>;
@@ -555,11 +568,6 @@ __global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int n) {
       S.flagA[b] = 1;
     }
     return;
-  }
-  for (int l = 0; l < k * NC; ++l) {
-    double s = 0.0;
-    for (int t = 0; t < nt; ++t) s += rec[t * RL + 3 + l];
-    rec[3 + l] = s;
   }
   V *pool = static_cast<V *>(S.pool);
   const V pv = pool[J.pe + h + bidx];
@@ -617,16 +625,14 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
   // cross terms Re(vdot(u_l, u) vdot(v_l, v)) with v_l = r_l / p_l, v = r / p:
   // vdot(v_l, v) = vdot(r_l, r) / (conj(p_l) p)
   const V *pool = static_cast<const V *>(S.pool);
-  const double *rdots = S.rpart + S.rowpart[b] + 3;
+  const double *rrec = S.rpart + S.rowpart[b];
+  const int ntr = tiles_of(w);
   const long long *tl = S.terms + (long long)b * S.tmax;
   double cross = 0.0;
   for (int l = 0; l < k; ++l) {
-    double ur = 0.0, ui = 0.0;
-    for (int t = 0; t < ntc; ++t) {
-      ur += crec[t * RL + 3 + (long long)l * NC];
-      if (C) ui += crec[t * RL + 3 + (long long)l * NC + 1];
-    }
-    const double vr = rdots[(long long)l * NC], vi = C ? rdots[(long long)l * NC + 1] : 0.0;
+    double ur, ui, vr, vi;
+    sum_dots<NC>(crec, ntc, RL, l, ur, ui);
+    sum_dots<NC>(rrec, ntr, RL, l, vr, vi);
     const V pl = pool[tl[l] + h + w];
     const double plr = (double)N::re(pl), pli = (double)N::im(pl);
     const double dr = plr * pr + pli * pim, di = plr * pim - pli * pr;  // conj(p_l) p
@@ -721,6 +727,7 @@ int aca_phase(const Prob<T> &P, AcaDev &S, const PhaseArgs &A, int op, bool helm
   HB_CUDA(cudaGetLastError());
   if (n_items > 0) {
     const unsigned grid = (unsigned)((n_items + kWarps - 1) / kWarps);
+    if (A.int_beg) HB_CUDA(cudaEventRecord(A.int_beg, st));
     int rc = dispatch_op(op, helm, nt, ns, [&](auto OPc, auto Hc, auto NTc, auto NSc) -> int {
       constexpr int OP = decltype(OPc)::value;
       constexpr bool HH = decltype(Hc)::value != 0;
@@ -742,6 +749,7 @@ int aca_phase(const Prob<T> &P, AcaDev &S, const PhaseArgs &A, int op, bool helm
       }
     });
     if (rc != HBEM_OK) return rc;
+    if (A.int_end) HB_CUDA(cudaEventRecord(A.int_end, st));
   }
   const unsigned fgrid = (unsigned)((n + kThreads - 1) / kThreads);
   if (col) k_fin_col<T, C><<<fgrid, kThreads, 0, st>>>(S, n);

@@ -27,6 +27,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -195,6 +197,8 @@ struct hbem_hmat {
   cudaStream_t hi = nullptr;    // ACA waves, highest priority
   cudaEvent_t side_done = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t iev[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // integration launches
+  bool int_pending[2] = {false, false};
   std::vector<void *> dev_allocs;
   hbem_hmat_stats stats{};
   double setup_s = 0.0;
@@ -212,6 +216,9 @@ struct hbem_hmat {
     if (side_done) cudaEventDestroy(side_done);
     for (auto e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto &pr : iev)
+      for (auto e : pr)
+        if (e) cudaEventDestroy(e);
   }
 };
 
@@ -299,7 +306,21 @@ template <typename T> Prob<T> make_prob(const hbem_hmat *H) {
 }
 
 // one-time: partition / DOF maps / ACA state / pools on the device
+// HBEM_TRACE=1: per-stage wall times of setup on stderr
+struct Trace {
+  bool on = std::getenv("HBEM_TRACE") != nullptr;
+  clk::time_point t = clk::now();
+  void mark(const char *what) {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    const auto n = clk::now();
+    std::fprintf(stderr, "[hbem setup] %-28s %8.3f s\n", what, secs(t, n));
+    t = n;
+  }
+};
+
 int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
+  Trace tr;
   hbem_ctx *ctx = H->ctx;
   const int64_t m = ctx->m;
   const int nt = ctx->nt, ns = ctx->ns;
@@ -368,6 +389,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   auto rng = [&](const int64_t *nodes, int64_t n) {
     return std::pair<int, int>((int)nodes[5 * n], (int)(nodes[5 * n + 1] - nodes[5 * n]));
   };
+  tr.mark("perms + records + incidence");
   // ---- admissible blocks --------------------------------------------------------
   const int na = (int)H->adm_leaf.size();
   H->na = na;
@@ -405,18 +427,16 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
     HB_CHECK(upload(H, &pl, rmo)); S.rmask_off = pl;
     HB_CHECK(upload(H, &pl, cmo)); S.cmask_off = pl;
     // static phase orders: row jobs grouped by column cluster, column jobs
-    // by row cluster (ties by block index: deterministic lists)
-    std::vector<int> order(na);
-    std::iota(order.begin(), order.end(), 0);
-    std::sort(order.begin(), order.end(), [&](int a, int b) {
-      return cnode[a] != cnode[b] ? cnode[a] < cnode[b] : a < b;
-    });
-    HB_CHECK(upload(H, &H->row_order, order));
-    std::iota(order.begin(), order.end(), 0);
-    std::sort(order.begin(), order.end(), [&](int a, int b) {
-      return rnode[a] != rnode[b] ? rnode[a] < rnode[b] : a < b;
-    });
-    HB_CHECK(upload(H, &H->col_order, order));
+    // by row cluster, ties by block index (counting sort: deterministic lists)
+    auto by_key = [&](const std::vector<int> &key, int64_t n_keys) {
+      std::vector<int> cnt(n_keys + 1, 0), order(na);
+      for (int q = 0; q < na; ++q) cnt[key[q] + 1]++;
+      for (int64_t k = 0; k < n_keys; ++k) cnt[k + 1] += cnt[k];
+      for (int q = 0; q < na; ++q) order[cnt[key[q]]++] = q;
+      return order;
+    };
+    HB_CHECK(upload(H, &H->row_order, by_key(cnode, d->n_col_nodes)));
+    HB_CHECK(upload(H, &H->col_order, by_key(rnode, d->n_row_nodes)));
   }
   HB_CHECK(dalloc(H, &S.rank, na));
   HB_CHECK(dalloc(H, &S.cur, na));
@@ -449,6 +469,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   H->cub_bytes = aca_cub_bytes(na);
   HB_CHECK(dalloc(H, (char **)&H->cub_tmp, H->cub_bytes));
   HB_CUDA(cudaMallocHost(&H->mail, sizeof(hbem_hmat::Mail)));
+  tr.mark("admissible blocks");
   // ---- near-field leaves --------------------------------------------------------
   const int nd = (int)H->den_leaf.size();
   H->nd = nd;
@@ -480,6 +501,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
       // touching element pairs integrated once per execute into a table the
       // near-field kernel reads (single layer: each unordered pair once)
       SingTable tab;
+      tr.mark("near-field arrays");
       HB_CHECK(build_sing_table(ctx->elem, (int)m, (int)ctx->nv, ctx->op == HBEM_SLP, tab,
                                 H->dev_allocs, 0));
       D.nb_ptr = tab.nb_ptr;
@@ -489,6 +511,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
       char *st_vals = nullptr;
       HB_CHECK(dalloc(H, &st_vals, (size_t)tab.nnz * H->vbytes));
       D.stab = st_vals;
+      tr.mark("singular table topology");
     }
     if (H->p0) {
       // warp items (leaf, 32-column tile); touching pairs read from the table
@@ -518,6 +541,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   const size_t vb = H->vbytes;
   HB_CUDA(cudaMalloc(&H->dense_nf, std::max<size_t>((size_t)tot * vb, vb)));
   H->D.out = H->dense_nf;
+  tr.mark("near-field leaves");
   // ---- factor pool: what is left after a margin for the admissible-dense arena
   size_t free_b = 0, total_b = 0;
   HB_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -526,6 +550,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   size_t cap_b = free_b > reserve ? free_b - reserve : 0;
   cap_b = std::min(cap_b, std::max(want, (size_t)1 << 20));
   HB_CUDA(cudaMalloc(&H->pool, std::max<size_t>(cap_b, vb)));
+  tr.mark("factor pool");
   S.pool = H->pool;
   S.pool_cap = (long long)(cap_b / vb);
   {
@@ -539,6 +564,8 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   }
   HB_CUDA(cudaEventCreateWithFlags(&H->side_done, cudaEventDisableTiming));
   for (auto &e : H->ev) HB_CUDA(cudaEventCreate(&e));
+  for (auto &pr : H->iev)
+    for (auto &e : pr) HB_CUDA(cudaEventCreate(&e));
   return HBEM_OK;
 }
 
@@ -585,6 +612,9 @@ int run_phase(hbem_hmat *H, const Prob<T> &P, int col, long long &pool_top, int 
     HB_CHECK(ensure(&H->partA, &H->partA_cap, (size_t)tot.part));
     S.part = H->partA;
   }
+  A.int_beg = H->iev[col][0];
+  A.int_end = H->iev[col][1];
+  H->int_pending[col] = tot.items > 0;
   return aca_phase<T, C>(P, S, A, ctx->op, ctx->helm, H->nt, H->ns, n, tot.items, st);
 }
 
@@ -662,6 +692,14 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
       float ms = 0.f;
       HB_CUDA(cudaEventElapsedTime(&ms, H->ev[0], H->ev[1]));
       ST.aca_kernel_ms += ms;
+      for (int ph = 0; ph < 2; ++ph)
+        if (H->int_pending[ph]) {
+          float im = 0.f;
+          HB_CUDA(cudaEventElapsedTime(&im, H->iev[ph][0], H->iev[ph][1]));
+          ST.int_kernel_ms += im;
+          ST.int_launches += 1;
+          H->int_pending[ph] = false;
+        }
       ST.row_jobs += nA;
       ST.col_jobs += nC;
       ++waves;
@@ -930,70 +968,112 @@ int hbem_hmat_copy_arenas(const hbem_hmat *hc, void *u, void *v, void *dense) {
   if (!h) return set_error(HBEM_ERR_ARG, "null hmat");
   HB_CUDA(cudaSetDevice(h->device));
   const size_t vb = h->vbytes;
+  // three streams: dense arenas straight to the host, and the factor records
+  // gathered into two alternating staging buffers so packing chunk i + 1
+  // overlaps the PCIe copy of chunk i
+  cudaStream_t sd = nullptr, sp[2] = {nullptr, nullptr};
+  HB_CUDA(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+  HB_CUDA(cudaStreamCreateWithFlags(&sp[0], cudaStreamNonBlocking));
+  HB_CUDA(cudaStreamCreateWithFlags(&sp[1], cudaStreamNonBlocking));
+  std::vector<void *> tmp;
+  auto done = [&]() {
+    cudaStreamSynchronize(sd);
+    cudaStreamSynchronize(sp[0]);
+    cudaStreamSynchronize(sp[1]);
+    for (void *q : tmp) cudaFree(q);
+    cudaStreamDestroy(sd);
+    cudaStreamDestroy(sp[0]);
+    cudaStreamDestroy(sp[1]);
+  };
+  auto fail = [&](cudaError_t e) {
+    done();
+    return set_error(HBEM_ERR_CUDA, "CUDA error %s in copy_arenas: %s", cudaGetErrorName(e),
+                     cudaGetErrorString(e));
+  };
+  cudaError_t e = cudaSuccess;
   if (dense) {
     if (h->nf_entries > 0)
-      HB_CUDA(cudaMemcpy(dense, h->dense_nf, (size_t)h->nf_entries * vb, cudaMemcpyDeviceToHost));
+      e = cudaMemcpyAsync(dense, h->dense_nf, (size_t)h->nf_entries * vb, cudaMemcpyDeviceToHost,
+                          sd);
     const long long adm = h->dense_entries - h->nf_entries;
-    if (adm > 0)
-      HB_CUDA(cudaMemcpy((char *)dense + (size_t)h->nf_entries * vb, h->dense_adm, (size_t)adm * vb,
-                         cudaMemcpyDeviceToHost));
+    if (e == cudaSuccess && adm > 0)
+      e = cudaMemcpyAsync((char *)dense + (size_t)h->nf_entries * vb, h->dense_adm,
+                          (size_t)adm * vb, cudaMemcpyDeviceToHost, sd);
+    if (e != cudaSuccess) return fail(e);
   }
   if ((u || v) && !h->lowrank_slots.empty()) {
-    // gather the factor records of the low-rank blocks in chunks
     const size_t n = h->lowrank_slots.size();
-    const long long chunk_vals = 64ll << 20;
-    void *su = nullptr, *sv = nullptr;
-    HB_CUDA(cudaMalloc(&su, chunk_vals * vb));
-    HB_CUDA(cudaMalloc(&sv, chunk_vals * vb));
+    const long long chunk_vals = 32ll << 20;
     int *d_slots = nullptr;
     long long *d_uo = nullptr, *d_vo = nullptr;
-    HB_CUDA(cudaMalloc(&d_slots, n * 4));
-    HB_CUDA(cudaMalloc(&d_uo, n * 8));
-    HB_CUDA(cudaMalloc(&d_vo, n * 8));
-    HB_CUDA(cudaMemcpy(d_slots, h->lowrank_slots.data(), n * 4, cudaMemcpyHostToDevice));
-    HB_CUDA(cudaMemcpy(d_uo, h->lr_uoff.data(), n * 8, cudaMemcpyHostToDevice));
-    HB_CUDA(cudaMemcpy(d_vo, h->lr_voff.data(), n * 8, cudaMemcpyHostToDevice));
+    void *su[2] = {nullptr, nullptr}, *sv[2] = {nullptr, nullptr};
+    long long cap[2] = {chunk_vals, chunk_vals};
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+      e = cudaMalloc(&su[b], chunk_vals * vb);
+      if (e == cudaSuccess) { tmp.push_back(su[b]); e = cudaMalloc(&sv[b], chunk_vals * vb); }
+      if (e == cudaSuccess) tmp.push_back(sv[b]);
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&d_slots, n * 4);
+    if (e == cudaSuccess) { tmp.push_back(d_slots); e = cudaMalloc(&d_uo, n * 8); }
+    if (e == cudaSuccess) { tmp.push_back(d_uo); e = cudaMalloc(&d_vo, n * 8); }
+    if (e == cudaSuccess) tmp.push_back(d_vo);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(d_slots, h->lowrank_slots.data(), n * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_uo, h->lr_uoff.data(), n * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_vo, h->lr_voff.data(), n * 8, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(e);
     size_t q0 = 0;
+    int buf = 0;
     while (q0 < n) {
       const long long ub = h->lr_uoff[q0], vbase = h->lr_voff[q0];
       size_t q1 = q0 + 1;
-      while (q1 < n && h->lr_uoff[q1] - ub < chunk_vals && h->lr_voff[q1] - vbase < chunk_vals &&
-             (q1 + 1 < n ? h->lr_uoff[q1 + 1] : h->u_entries) - ub <= chunk_vals &&
+      while (q1 < n && (q1 + 1 < n ? h->lr_uoff[q1 + 1] : h->u_entries) - ub <= chunk_vals &&
              (q1 + 1 < n ? h->lr_voff[q1 + 1] : h->v_entries) - vbase <= chunk_vals)
         ++q1;
       const long long ue = q1 < n ? h->lr_uoff[q1] : h->u_entries;
       const long long ve = q1 < n ? h->lr_voff[q1] : h->v_entries;
-      if (ue - ub > chunk_vals || ve - vbase > chunk_vals) {
-        cudaFree(su); cudaFree(sv);
-        HB_CUDA(cudaMalloc(&su, (ue - ub) * vb));
-        HB_CUDA(cudaMalloc(&sv, (ve - vbase) * vb));
+      cudaStream_t st = sp[buf];
+      const long long need = std::max(ue - ub, ve - vbase);
+      if (need > cap[buf]) {  // one oversized block: private staging
+        e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess) e = cudaMalloc(&su[buf], need * vb);
+        if (e == cudaSuccess) { tmp.push_back(su[buf]); e = cudaMalloc(&sv[buf], need * vb); }
+        if (e == cudaSuccess) { tmp.push_back(sv[buf]); cap[buf] = need; }
+        if (e != cudaSuccess) return fail(e);
       }
       const int cnt = (int)(q1 - q0);
       if (h->vbytes == 16)
-        k_pack_factors<double, true><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0,
-                                                 ub, vbase, (Cx<double> *)su, (Cx<double> *)sv);
+        k_pack_factors<double, true><<<cnt, 128, 0, st>>>(d_slots + q0, cnt, h->S, d_uo + q0,
+                                                          d_vo + q0, ub, vbase,
+                                                          (Cx<double> *)su[buf],
+                                                          (Cx<double> *)sv[buf]);
       else if (h->vbytes == 8 && h->complex_)
-        k_pack_factors<float, true><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
-                                                vbase, (Cx<float> *)su, (Cx<float> *)sv);
+        k_pack_factors<float, true><<<cnt, 128, 0, st>>>(d_slots + q0, cnt, h->S, d_uo + q0,
+                                                         d_vo + q0, ub, vbase,
+                                                         (Cx<float> *)su[buf],
+                                                         (Cx<float> *)sv[buf]);
       else if (h->vbytes == 8)
-        k_pack_factors<double, false><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
-                                             vbase, (double *)su, (double *)sv);
+        k_pack_factors<double, false><<<cnt, 128, 0, st>>>(d_slots + q0, cnt, h->S, d_uo + q0,
+                                                           d_vo + q0, ub, vbase,
+                                                           (double *)su[buf], (double *)sv[buf]);
       else
-        k_pack_factors<float, false><<<cnt, 128>>>(d_slots + q0, cnt, h->S, d_uo + q0, d_vo + q0, ub,
-                                            vbase, (float *)su, (float *)sv);
-      HB_CUDA(cudaGetLastError());
-      if (u)
-        HB_CUDA(cudaMemcpy((char *)u + ub * vb, su, (ue - ub) * vb, cudaMemcpyDeviceToHost));
-      if (v)
-        HB_CUDA(cudaMemcpy((char *)v + vbase * vb, sv, (ve - vbase) * vb, cudaMemcpyDeviceToHost));
+        k_pack_factors<float, false><<<cnt, 128, 0, st>>>(d_slots + q0, cnt, h->S, d_uo + q0,
+                                                          d_vo + q0, ub, vbase, (float *)su[buf],
+                                                          (float *)sv[buf]);
+      e = cudaGetLastError();
+      if (e == cudaSuccess && u)
+        e = cudaMemcpyAsync((char *)u + ub * vb, su[buf], (ue - ub) * vb, cudaMemcpyDeviceToHost,
+                            st);
+      if (e == cudaSuccess && v)
+        e = cudaMemcpyAsync((char *)v + vbase * vb, sv[buf], (ve - vbase) * vb,
+                            cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) return fail(e);
       q0 = q1;
+      buf ^= 1;
     }
-    cudaFree(su);
-    cudaFree(sv);
-    cudaFree(d_slots);
-    cudaFree(d_uo);
-    cudaFree(d_vo);
   }
+  done();
+  HB_CUDA(cudaGetLastError());
   return HBEM_OK;
 }
 

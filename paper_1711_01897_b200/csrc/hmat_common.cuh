@@ -14,7 +14,16 @@
 
 #include "hbem_internal.h"
 
+#ifndef HB_INNER_UNROLL2
+#define HB_INNER_UNROLL2 2  // fixed-point loop unroll of the two-job quadrature
+#endif
+#ifndef HB_ACA_MINB
+#define HB_ACA_MINB 3  // k_aca_p0 / k_near_p0 resident CTAs per SM (register cap)
+#endif
+
 namespace hb {
+
+constexpr int kInnerUnroll2 = HB_INNER_UNROLL2;
 
 // ---------------------------------------------------------------------------
 // value arithmetic (real T or complex as (re, im) pairs, numpy layout)
@@ -258,7 +267,7 @@ __device__ __forceinline__ void p0_pairs_fx(const RuleTab<T> &R, const ElemRec<T
     T ar[NJ], ai[NJ];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) { ar[j] = T(0); ai[j] = T(0); }
-#pragma unroll(NJ == 1 ? 2 : 1)
+#pragma unroll(NJ == 1 ? 2 : kInnerUnroll2)
     for (int o = 0; o < 6; ++o) {
       const T wo = FIXED_TEST ? R.wa[0][o] : R.wb[0][o];
 #pragma unroll
@@ -444,6 +453,7 @@ struct PhaseArgs {
   void *cub_tmp;
   size_t cub_bytes;
   int *sel_tmp;       // na flags scratch for the compaction
+  cudaEvent_t int_beg, int_end;  // recorded around the integration launch (may be null)
 };
 
 template <typename T, bool C>

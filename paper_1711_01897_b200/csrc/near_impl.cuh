@@ -35,7 +35,7 @@ __global__ void k_build_recs(Geo<T> g, const int4 *elem, const int *perm, int n,
 }
 
 template <typename T, bool C, int OP, bool HELM>
-__global__ void __launch_bounds__(kThreads, 4) k_near_p0(Prob<T> P, DenseDev D) {
+__global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_near_p0(Prob<T> P, DenseDev D) {
   using N = Num<T, C>;
   using V = typename N::V;
   constexpr unsigned kAll = 0xffffffffu;
