@@ -159,14 +159,25 @@ def _oracle_setup(v, e, bt, eps, precision):
     _G["asm"] = O.Assembler(P, tree, tree, leaves, eps)
 
 
-def _oracle_leaves(ids):
+def _oracle_leaves(ids, seconds=None):
+    """Assemble leaves ``ids`` in order with the oracle, stopping after
+    ``seconds`` of work if given; returns (wall, regular, singular, done)."""
     asm = _G["asm"]
     asm.counters.update({"regular_pairs": 0, "singular_pairs": 0})
     t0 = time.perf_counter()
+    done = 0
     for ix in ids:
         asm.leaf(int(ix))
+        done += 1
+        if seconds is not None and time.perf_counter() - t0 >= seconds:
+            break
     return (time.perf_counter() - t0, asm.counters["regular_pairs"],
-            asm.counters["singular_pairs"])
+            asm.counters["singular_pairs"], done)
+
+
+def _oracle_worker(arg):
+    ids, seconds = arg
+    return _oracle_leaves(ids, seconds)
 
 
 def cpu_sample_ids(bt, n, rng):
@@ -177,31 +188,22 @@ def cpu_sample_ids(bt, n, rng):
 
 
 def cpu_rate(bt, seconds, workers, rng):
-    """Assemble cost-weighted random leaves for about ``seconds`` per worker;
-    returns (pairs/s, regular, singular, leaves, wall)."""
+    """Assemble cost-weighted random leaves for about ``seconds`` per worker
+    (every worker stops after its time budget); returns (pairs/s, regular,
+    singular, leaves, wall) with wall = the slowest worker."""
     ids = cpu_sample_ids(bt, 200000, rng)
     if workers <= 1:
-        done, reg, sing, t_all, k = 0, 0, 0, 0.0, 0
-        t0 = time.perf_counter()
-        while time.perf_counter() - t0 < seconds and k < len(ids):
-            dt, r, s = _oracle_leaves(ids[k:k + 8])
-            reg, sing, t_all, k = reg + r, sing + s, t_all + dt, k + 8
-        wall = time.perf_counter() - t0
-        return (reg + sing) / wall, reg, sing, k, wall
+        wall, reg, sing, done = _oracle_leaves(ids, seconds)
+        return (reg + sing) / wall, reg, sing, done, wall
     import multiprocessing as mp
     ctx = mp.get_context("fork")
-    # calibrate batch size on one process, then give every worker equal work
-    dt, r, s = _oracle_leaves(ids[:16])
-    per_leaf = max(dt / 16, 1e-4)
-    nper = max(8, int(seconds / per_leaf))
-    chunks = [ids[16 + i * nper: 16 + (i + 1) * nper] for i in range(workers)]
-    t0 = time.perf_counter()
+    chunks = [(ids[i::workers], seconds) for i in range(workers)]
     with ctx.Pool(workers) as pool:
-        res = pool.map(_oracle_leaves, chunks)
-    wall = time.perf_counter() - t0
+        res = pool.map(_oracle_worker, chunks)
+    wall = max(x[0] for x in res)
     reg = sum(x[1] for x in res)
     sing = sum(x[2] for x in res)
-    return (reg + sing) / wall, reg, sing, sum(len(c) for c in chunks), wall
+    return (reg + sing) / wall, reg, sing, sum(x[3] for x in res), wall
 
 
 def run_reference(args):
@@ -213,17 +215,17 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     _oracle_setup(v, e, bt, args.eps, args.precision)
     rng = np.random.default_rng(1234)
-    per_step = max(5.0, min(args.cpu_seconds, 20.0))
+    per_step = max(2.0, min(args.cpu_seconds, 20.0))
     for _ in range(args.warmup):
-        cpu_rate(bt, per_step / 4, cores, rng)
+        cpu_rate(bt, min(per_step / 4, 2.0), cores, rng)
     rates, times = [], []
     for _ in range(args.steps):
         rate, reg, sing, nl, wall = cpu_rate(bt, per_step, cores, rng)
         rates.append(rate)
         times.append(wall)
     rate = float(np.median(rates))
-    sample = (f"{nl} leaves per step drawn cost-weighted from the {len(bt.leaf_array)} C5 "
-              f"leaves; oracle (numpy restatement of hbem.hmatrix.aca/_row_job/_col_job/"
+    sample = (f"{nl} leaves per step ({per_step:g} s per process) drawn cost-weighted from the "
+              f"{len(bt.leaf_array)} C5 leaves; oracle (numpy restatement of hbem.hmatrix.aca/_row_job/_col_job/"
               f"dense_leaf + integrate_batch + local_matrix) on {cores} processes")
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

@@ -22,6 +22,8 @@
 // (hmatrix.py:721-735): converged and rank (h + w) < h w -> low rank,
 // converged otherwise -> dense u v^T, rank cap without convergence -> dense
 // exact rows.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -145,6 +147,101 @@ using namespace hb;
 // host side: setup (partition upload, index structures) and execute (one
 // complete assembly: record gather, near-field leaves, ACA waves, payloads)
 // ---------------------------------------------------------------------------
+// Growable device pool on the CUDA virtual memory API: a large virtual range
+// is reserved once and physical memory is mapped in 2 GiB steps as the ACA
+// waves need it, so the factor pool occupies what the assembly actually
+// stores (a few % over the payload) instead of a worst-case estimate.
+// driver-API entry points resolved through the runtime (no link-time
+// dependency on libcuda, so the library still loads on GPU-less hosts)
+struct VmmApi {
+  PFN_cuMemGetAllocationGranularity granularity = nullptr;
+  PFN_cuMemAddressReserve reserve = nullptr;
+  PFN_cuMemAddressFree address_free = nullptr;
+  PFN_cuMemCreate create = nullptr;
+  PFN_cuMemRelease release = nullptr;
+  PFN_cuMemMap map = nullptr;
+  PFN_cuMemUnmap unmap = nullptr;
+  PFN_cuMemSetAccess set_access = nullptr;
+  bool load() {
+    if (create) return true;
+    auto get = [](const char *name, void **fn) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess && *fn;
+    };
+    return get("cuMemGetAllocationGranularity", (void **)&granularity) &&
+           get("cuMemAddressReserve", (void **)&reserve) &&
+           get("cuMemAddressFree", (void **)&address_free) &&
+           get("cuMemCreate", (void **)&create) && get("cuMemRelease", (void **)&release) &&
+           get("cuMemMap", (void **)&map) && get("cuMemUnmap", (void **)&unmap) &&
+           get("cuMemSetAccess", (void **)&set_access);
+  }
+};
+static VmmApi g_vmm;
+
+struct VPool {
+  CUdeviceptr base = 0;
+  size_t reserved = 0, mapped = 0, step = 0;
+  std::vector<CUmemGenericAllocationHandle> handles;
+  std::vector<size_t> sizes;
+  CUmemAllocationProp prop{};
+  int dev = 0;
+  int init(int device, size_t reserve_bytes) {
+    dev = device;
+    if (!g_vmm.load()) return set_error(HBEM_ERR_CUDA, "CUDA virtual memory API unavailable");
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = device;
+    size_t gran = 0;
+    if (g_vmm.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) !=
+        CUDA_SUCCESS)
+      return set_error(HBEM_ERR_CUDA, "cuMemGetAllocationGranularity failed");
+    step = std::max<size_t>(gran, (size_t)2 << 30);
+    step = (step + gran - 1) / gran * gran;
+    reserved = (reserve_bytes + step - 1) / step * step;
+    if (g_vmm.reserve(&base, reserved, 0, 0, 0) != CUDA_SUCCESS)
+      return set_error(HBEM_ERR_CAPACITY, "cannot reserve %zu bytes of device address space",
+                       reserved);
+    return HBEM_OK;
+  }
+  // map until at least `bytes` are backed
+  int grow(size_t bytes) {
+    while (mapped < bytes) {
+      if (mapped + step > reserved)
+        return set_error(HBEM_ERR_CAPACITY, "ACA factor pool exhausted (%zu bytes reserved)",
+                         reserved);
+      CUmemGenericAllocationHandle hnd;
+      if (g_vmm.create(&hnd, step, &prop, 0) != CUDA_SUCCESS)
+        return set_error(HBEM_ERR_CAPACITY,
+                         "device memory exhausted growing the ACA factor pool to %zu bytes",
+                         mapped + step);
+      if (g_vmm.map(base + mapped, step, 0, hnd, 0) != CUDA_SUCCESS) {
+        g_vmm.release(hnd);
+        return set_error(HBEM_ERR_CUDA, "cuMemMap failed");
+      }
+      CUmemAccessDesc acc{};
+      acc.location = prop.location;
+      acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+      if (g_vmm.set_access(base + mapped, step, &acc, 1) != CUDA_SUCCESS)
+        return set_error(HBEM_ERR_CUDA, "cuMemSetAccess failed");
+      handles.push_back(hnd);
+      sizes.push_back(step);
+      mapped += step;
+    }
+    return HBEM_OK;
+  }
+  ~VPool() {
+    if (!base) return;
+    size_t off = 0;
+    for (size_t i = 0; i < handles.size(); ++i) {
+      g_vmm.unmap(base + off, sizes[i]);
+      g_vmm.release(handles[i]);
+      off += sizes[i];
+    }
+    g_vmm.address_free(base, reserved);
+  }
+};
+
 struct hbem_hmat {
   hbem_ctx *ctx = nullptr;
   int device = 0;
@@ -176,7 +273,7 @@ struct hbem_hmat {
   size_t partA_cap = 0, partC_cap = 0;  // doubles
   long long items_cap = 0;
   AcaDev S{};
-  void *pool = nullptr;
+  VPool vpool;  // ACA factor pool
   // pinned mailbox for the per-phase host reads
   struct Mail { Need tot; int n; int pad; } *mail = nullptr;
   // near-field leaves
@@ -192,6 +289,15 @@ struct hbem_hmat {
   size_t dense_adm_cap = 0;
   long long dense_entries = 0, u_entries = 0, v_entries = 0;
   std::vector<int> lowrank_slots;
+  // matvec: admissible blocks stored densely (host lists, uploaded lazily)
+  std::vector<int> ad_r0, ad_c0, ad_h, ad_w;
+  std::vector<long long> ad_off, ad_rowbase;
+  long long nf_rows = 0;
+  const long long *nf_rowbase = nullptr;
+  bool mv_dirty = true;
+  void *mv_buf = nullptr;  // x, y, xt, yt
+  int *mv_lr = nullptr, *mv_ad = nullptr;
+  long long *mv_ad_l = nullptr;
   std::vector<int64_t> lr_uoff, lr_voff;
   cudaStream_t side = nullptr;  // near-field leaves, lowest priority
   cudaStream_t hi = nullptr;    // ACA waves, highest priority
@@ -205,11 +311,14 @@ struct hbem_hmat {
   ~hbem_hmat() {
     cudaSetDevice(device);
     for (void *p : dev_allocs) cudaFree(p);
-    cudaFree(pool);
     cudaFree(dense_nf);
     cudaFree(dense_adm);
     cudaFree(partA);
     cudaFree(partC);
+    cudaFree(mv_buf);
+    cudaFree(mv_lr);
+    cudaFree(mv_ad);
+    cudaFree(mv_ad_l);
     if (mail) cudaFreeHost(mail);
     if (side) cudaStreamDestroy(side);
     if (hi) cudaStreamDestroy(hi);
@@ -487,6 +596,15 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   }
   H->nf_entries = tot;
   {
+    std::vector<long long> rb(nd);
+    long long acc = 0;
+    for (int q = 0; q < nd; ++q) { rb[q] = acc; acc += dh[q]; }
+    H->nf_rows = acc;
+    long long *p;
+    HB_CHECK(upload(H, &p, rb));
+    H->nf_rowbase = p;
+  }
+  {
     DenseDev &D = H->D;
     int *p;
     long long *pl;
@@ -542,17 +660,15 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   HB_CUDA(cudaMalloc(&H->dense_nf, std::max<size_t>((size_t)tot * vb, vb)));
   H->D.out = H->dense_nf;
   tr.mark("near-field leaves");
-  // ---- factor pool: what is left after a margin for the admissible-dense arena
+  // ---- factor pool: virtual range of the free memory, mapped on demand
   size_t free_b = 0, total_b = 0;
+  HB_CUDA(cudaFree(nullptr));
   HB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const size_t want = (size_t)sum_hw * (size_t)std::min(S.tmax, 24) * vb;
-  const size_t reserve = ((size_t)6 << 30) + (size_t)(0.03 * (double)free_b);
-  size_t cap_b = free_b > reserve ? free_b - reserve : 0;
-  cap_b = std::min(cap_b, std::max(want, (size_t)1 << 20));
-  HB_CUDA(cudaMalloc(&H->pool, std::max<size_t>(cap_b, vb)));
+  HB_CHECK(H->vpool.init(H->device, std::max<size_t>(free_b, (size_t)4 << 30)));
+  (void)sum_hw;
   tr.mark("factor pool");
-  S.pool = H->pool;
-  S.pool_cap = (long long)(cap_b / vb);
+  S.pool = reinterpret_cast<void *>(H->vpool.base);
+  S.pool_cap = (long long)(H->vpool.reserved / vb);
   {
     // the ACA waves (latency-bound finalize phases, host reads between
     // phases) run on a high-priority stream; the compute-bound near-field
@@ -598,6 +714,7 @@ int run_phase(hbem_hmat *H, const Prob<T> &P, int col, long long &pool_top, int 
       return set_error(HBEM_ERR_CAPACITY,
                        "ACA factor pool of %lld values exhausted at wave %d (need %lld more)",
                        (long long)S.pool_cap, wave, (long long)(pool_top + tot.pool - S.pool_cap));
+    HB_CHECK(H->vpool.grow((size_t)(pool_top + tot.pool) * H->vbytes));
     S.pool_base = pool_top;
     pool_top += tot.pool;
   }
@@ -764,6 +881,22 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
     adm_dense += hw;
   }
   ST.dense_leaves = H->nd + (int64_t)expand_slots.size() + (int64_t)fb_r0.size();
+  H->ad_r0.clear(); H->ad_c0.clear(); H->ad_h.clear(); H->ad_w.clear();
+  H->ad_off.clear(); H->ad_rowbase.clear();
+  {
+    long long rows = 0;
+    auto add = [&](int q, long long off) {
+      H->ad_r0.push_back(H->ar0[q]); H->ad_c0.push_back(H->ac0[q]);
+      H->ad_h.push_back(H->ah[q]); H->ad_w.push_back(H->aw[q]);
+      H->ad_off.push_back(off); H->ad_rowbase.push_back(rows);
+      rows += H->ah[q];
+    };
+    for (size_t z = 0; z < expand_slots.size(); ++z) add(expand_slots[z], expand_off[z]);
+    size_t fz = 0;
+    for (int q = 0; q < na && fz < fb_off.size(); ++q)
+      if (st_h[q] != ST_CONVERGED) add(q, fb_off[fz++]);
+  }
+  H->mv_dirty = true;
   H->dense_entries = H->nf_entries + adm_dense;
   const size_t vb = sizeof(V);
   if ((size_t)adm_dense * vb > H->dense_adm_cap) {
@@ -1077,8 +1210,61 @@ int hbem_hmat_copy_arenas(const hbem_hmat *hc, void *u, void *v, void *dense) {
   return HBEM_OK;
 }
 
-int hbem_hmat_matvec(const hbem_hmat *, const void *, void *) {
-  return set_error(HBEM_ERR_CONFIG, "device matvec not available in this build");
+int hbem_hmat_matvec(const hbem_hmat *hc, const void *x, void *y) {
+  clear_error();
+  hbem_hmat *h = const_cast<hbem_hmat *>(hc);
+  if (!h || !x || !y) return set_error(HBEM_ERR_ARG, "null argument");
+  HB_CUDA(cudaSetDevice(h->device));
+  const size_t vb = h->vbytes;
+  const int nr = h->n_rows, nc = h->n_cols;
+  if (!h->mv_buf) HB_CUDA(cudaMalloc(&h->mv_buf, (size_t)2 * (nr + nc) * vb));
+  char *buf = static_cast<char *>(h->mv_buf);
+  void *dx = buf, *dxt = buf + (size_t)nc * vb, *dy = buf + (size_t)2 * nc * vb,
+       *dyt = buf + (size_t)(2 * nc + nr) * vb;
+  if (h->mv_dirty) {
+    cudaFree(h->mv_lr); cudaFree(h->mv_ad); cudaFree(h->mv_ad_l);
+    h->mv_lr = nullptr; h->mv_ad = nullptr; h->mv_ad_l = nullptr;
+    const size_t nl = h->lowrank_slots.size(), na = h->ad_r0.size();
+    HB_CUDA(cudaMalloc(&h->mv_lr, std::max<size_t>(nl, 1) * 4));
+    HB_CUDA(cudaMalloc(&h->mv_ad, std::max<size_t>(na, 1) * 4 * 4));
+    HB_CUDA(cudaMalloc(&h->mv_ad_l, std::max<size_t>(na, 1) * 8 * 2));
+    if (nl) HB_CUDA(cudaMemcpy(h->mv_lr, h->lowrank_slots.data(), nl * 4, cudaMemcpyHostToDevice));
+    if (na) {
+      HB_CUDA(cudaMemcpy(h->mv_ad, h->ad_r0.data(), na * 4, cudaMemcpyHostToDevice));
+      HB_CUDA(cudaMemcpy(h->mv_ad + na, h->ad_c0.data(), na * 4, cudaMemcpyHostToDevice));
+      HB_CUDA(cudaMemcpy(h->mv_ad + 2 * na, h->ad_h.data(), na * 4, cudaMemcpyHostToDevice));
+      HB_CUDA(cudaMemcpy(h->mv_ad + 3 * na, h->ad_w.data(), na * 4, cudaMemcpyHostToDevice));
+      HB_CUDA(cudaMemcpy(h->mv_ad_l, h->ad_off.data(), na * 8, cudaMemcpyHostToDevice));
+      HB_CUDA(cudaMemcpy(h->mv_ad_l + na, h->ad_rowbase.data(), na * 8, cudaMemcpyHostToDevice));
+    }
+    h->mv_dirty = false;
+  }
+  MatvecArgs M{};
+  M.n_rows = nr;
+  M.n_cols = nc;
+  M.rperm = h->rperm;
+  M.cperm = h->cperm;
+  M.x = dx; M.y = dy; M.xt = dxt; M.yt = dyt;
+  M.dense[0] = MatvecArgs::Dense{h->nd, h->D.r0, h->D.c0, h->D.h, h->D.w, h->D.off,
+                                 h->nf_rowbase, h->nf_rows, h->dense_nf};
+  const int na = (int)h->ad_r0.size();
+  long long ad_rows = 0;
+  for (int hh : h->ad_h) ad_rows += hh;
+  M.dense[1] = MatvecArgs::Dense{na, h->mv_ad, h->mv_ad + na, h->mv_ad + 2 * na,
+                                 h->mv_ad + 3 * na, h->mv_ad_l, h->mv_ad_l + na, ad_rows,
+                                 h->dense_adm};
+  M.n_lowrank = (int)h->lowrank_slots.size();
+  M.lowrank = h->mv_lr;
+  HB_CUDA(cudaMemcpy(dx, x, (size_t)nc * vb, cudaMemcpyHostToDevice));
+  const hbem_ctx *ctx = h->ctx;
+  int rc;
+  if (ctx->precision == HBEM_DOUBLE)
+    rc = ctx->helm ? matvec_launch<double, true>(M, h->S, 0) : matvec_launch<double, false>(M, h->S, 0);
+  else
+    rc = ctx->helm ? matvec_launch<float, true>(M, h->S, 0) : matvec_launch<float, false>(M, h->S, 0);
+  if (rc != HBEM_OK) return rc;
+  HB_CUDA(cudaMemcpy(y, dy, (size_t)nr * vb, cudaMemcpyDeviceToHost));
+  return HBEM_OK;
 }
 
 int hbem_hmat_destroy(hbem_hmat *h) {

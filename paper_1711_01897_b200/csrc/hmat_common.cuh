@@ -469,6 +469,24 @@ size_t aca_cub_bytes(int na);
 
 template <typename T>
 int build_recs(const Geo<T> &g, const int4 *elem, const int *perm, int n, T *recs, cudaStream_t st);
+struct MatvecArgs {
+  int n_rows, n_cols;
+  const int *rperm, *cperm;
+  const void *x;  // device, original DOF order
+  void *y;        // device, original DOF order
+  void *xt, *yt;  // device scratch, tree order
+  struct Dense {
+    int n;
+    const int *r0, *c0, *h, *w;
+    const long long *off, *rowbase;
+    long long nrows;
+    const void *arena;
+  } dense[2];     // near-field leaves, admissible blocks stored densely
+  int n_lowrank;
+  const int *lowrank;  // admissible block slots
+};
+template <typename T, bool C>
+int matvec_launch(const MatvecArgs &M, const AcaDev &S, cudaStream_t st);
 template <typename T, bool C>
 int sing_table_launch(const Prob<T> &P, const DenseDev &D, int op, bool helm, cudaStream_t st);
 template <typename T, bool C>

@@ -1,6 +1,7 @@
 // float32 instantiation of the ACA wave and P0 near-field kernels.
 #include "aca_impl.cuh"
 #include "near_impl.cuh"
+#include "matvec_impl.cuh"
 
 namespace hb {
 
@@ -24,4 +25,6 @@ template int sing_table_launch<float, false>(const Prob<float> &, const DenseDev
                                              cudaStream_t);
 template int sing_table_launch<float, true>(const Prob<float> &, const DenseDev &, int, bool,
                                             cudaStream_t);
+template int matvec_launch<float, false>(const MatvecArgs &, const AcaDev &, cudaStream_t);
+template int matvec_launch<float, true>(const MatvecArgs &, const AcaDev &, cudaStream_t);
 }  // namespace hb

@@ -1,6 +1,7 @@
 // float64 instantiation of the ACA wave and P0 near-field kernels.
 #include "aca_impl.cuh"
 #include "near_impl.cuh"
+#include "matvec_impl.cuh"
 
 namespace hb {
 size_t aca_cub_bytes(int na) { return aca_cub_bytes_impl(na); }
@@ -25,4 +26,6 @@ template int sing_table_launch<double, false>(const Prob<double> &, const DenseD
                                              cudaStream_t);
 template int sing_table_launch<double, true>(const Prob<double> &, const DenseDev &, int, bool,
                                             cudaStream_t);
+template int matvec_launch<double, false>(const MatvecArgs &, const AcaDev &, cudaStream_t);
+template int matvec_launch<double, true>(const MatvecArgs &, const AcaDev &, cudaStream_t);
 }  // namespace hb

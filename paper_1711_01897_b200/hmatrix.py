@@ -158,8 +158,9 @@ def pinned_empty(n: int, dtype) -> np.ndarray:
 class _DevicePart:
     """One hbem_hmat (one GPU's share of the leaves) and its host arenas."""
 
-    def __init__(self, handle, n_leaves, shapes, dtype):
+    def __init__(self, handle, n_leaves, shapes, dtype, n_rows=0):
         self.handle = handle
+        self.n_rows = n_rows
         self.dtype = dtype
         self.shapes = shapes  # (L, 2) h, w
         self.n_leaves = n_leaves
@@ -222,6 +223,13 @@ class _DevicePart:
         o = self.off_d[q]
         return DenseBlock(d[o: o + h * w].reshape(h, w))
 
+    def matvec(self, x: np.ndarray) -> np.ndarray:
+        """Device y = H_part x in original DOF order (x, y in the result dtype)."""
+        x = np.ascontiguousarray(x, dtype=self.dtype)
+        y = np.empty(self.n_rows, dtype=self.dtype)
+        check(lib.hbem_hmat_matvec(self.handle, _lib.vptr(x), _lib.vptr(y)))
+        return y
+
     def close(self):
         if self.handle:
             lib.hbem_hmat_destroy(self.handle)
@@ -267,13 +275,27 @@ class HMatrix:
         return out
 
 
-def hmat_matvec(h: HMatrix, x: np.ndarray) -> np.ndarray:
-    """y = H x in the original DOF ordering, leaves applied in fixed
-    (row.start, col.start) order (hmatrix.py:441-470)."""
+def hmat_matvec(h: HMatrix, x: np.ndarray, device: bool = True) -> np.ndarray:
+    """y = H x in the original DOF ordering (hmatrix.py:441-470).
+
+    ``device=True`` (default when the payloads are device-resident): one
+    ``hbem_hmat_matvec`` per GPU part straight from the device arenas,
+    summed over the parts.  ``device=False``: the host loop over the leaf
+    payloads in fixed (row.start, col.start) order, as the reference."""
     m, n = h.shape
     x = np.asarray(x)
     if x.shape != (n,):
         raise AssemblyError(f"matvec expects a vector of length {n}, got {x.shape}")
+    if device and h.parts and all(p.handle for _, p in h.parts):
+        rd = np.dtype(h.dtype)
+        if np.iscomplexobj(x) and rd.kind != "c":
+            return (hmat_matvec(h, x.real.copy(), True)
+                    + 1j * hmat_matvec(h, x.imag.copy(), True))
+        y = None
+        for _, part in h.parts:
+            yp = part.matvec(x.astype(rd, copy=False))
+            y = yp if y is None else y + yp
+        return y
     rows, cols = h.tree.rows, h.tree.cols
     xt = x[cols.permutation]
     yt = np.zeros(m, dtype=np.result_type(h.dtype, x.dtype))
@@ -369,7 +391,7 @@ def _assemble_part(dev_ctx, tree: BlockClusterTree, leaf_ids, test_space, trial_
     h = C.c_void_p()
     check(lib.hbem_hmat_assemble(dev_ctx.handle, C.byref(d), stream, C.byref(h)))
     shapes = np.stack([rn[la[:, 0], 1] - rn[la[:, 0], 0], cn[la[:, 1], 1] - cn[la[:, 1], 0]], 1)
-    return _DevicePart(h, len(la), shapes, dev_ctx.spec.result_dtype)
+    return _DevicePart(h, len(la), shapes, dev_ctx.spec.result_dtype, n_rows=len(rp))
 
 
 COUNTER_NAMES = ("host_jobs", "backend_jobs", "singular_pairs", "aca_converged", "aca_exhausted",

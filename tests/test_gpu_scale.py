@@ -1,0 +1,129 @@
+"""GPU parity at scale through size-independent properties.
+
+The reference cannot assemble 10^5-element H-matrices in test time, so the
+large cases are checked against exact operator rows computed on the GPU by
+the batched integrator (hbem_integrate_any = local_matrix over every pair),
+which itself is pinned to the reference at 1e-12 by tests/test_gpu_integrate.py:
+
+  * sampled rows of H x equal the exact (A x)_i within the ACA tolerance;
+  * device matvec == host leaf-by-leaf matvec (hmatrix.py:441-470) to rounding;
+  * two executes of one handle give bit-identical payloads (fixed reduction
+    order, deterministic job lists);
+  * FP32 assembly within 5e-4 of FP64 (FP32 is judged against FP64,
+    SURVEY §8a row 7).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def problem(n_or_mesh, fam, eq, op, k, prec="double"):
+    from paper_1711_01897_b200.discretization import OperatorSpec, TriangleMesh, build_space
+    from paper_1711_01897_b200.meshes import geodesic_sphere
+    from paper_1711_01897_b200.partition import cluster_trees_for
+    v, e = geodesic_sphere(n_or_mesh) if isinstance(n_or_mesh, int) else n_or_mesh
+    spec = OperatorSpec(eq, op, k, prec)
+    sp = build_space(TriangleMesh(v, e), fam)
+    return v, e, spec, sp, cluster_trees_for(sp, sp)
+
+
+def exact_rows(spec, sp, rows, x):
+    """(A x)_i for DOFs i: every element pair carrying test DOF i, integrated
+    by the GPU batched integrator (any adjacency), accumulated onto trial
+    DOFs with the dofmap (_row_job, hmatrix.py:625-649)."""
+    from paper_1711_01897_b200.backend import BatchRequest, make_gpu_backends
+    from paper_1711_01897_b200.discretization import make_integration_context
+    be = make_gpu_backends(make_integration_context(spec, sp, sp))[0]
+    dm = np.asarray(sp.dofmap).reshape(len(sp.dofmap), -1)
+    m = len(dm)
+    out = []
+    for i in rows:
+        els, locs = np.nonzero(dm == i)
+        acc = 0.0
+        for el, a in zip(els, locs):
+            pairs = np.stack([np.full(m, el), np.arange(m)], 1)
+            res = be.integrate_pairs(BatchRequest(pairs))
+            blk = res.complex_view()[:, a, :]           # (m, ns)
+            acc = acc + (blk * x[dm]).sum()
+        out.append(acc)
+    return np.array(out)
+
+
+@pytest.mark.parametrize("n,fam,eq,op,k,eps", [
+    (45, "p0", "laplace", "slp", 0.0, 1e-3),      # C2 mesh size, C5 operator
+    (100, "p0", "laplace", "slp", 0.0, 1e-3),     # 200 000 elements
+    (45, "p0", "helmholtz", "slp", 10.0, 1e-4),
+    (30, "p0", "laplace", "dlp", 0.0, 1e-4),
+    (20, "p1c", "laplace", "dlp", 0.0, 1e-4),     # C2 operator/space
+])
+def test_sampled_rows_vs_exact_operator(n, fam, eq, op, k, eps):
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix
+    v, e, spec, sp, bt = problem(n, fam, eq, op, k)
+    h = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=eps))
+    rng = np.random.default_rng(1234)
+    x = rng.standard_normal(sp.n_dofs)
+    y = h.matvec(x)
+    rows = rng.choice(sp.n_dofs, size=8, replace=False)
+    z = exact_rows(spec, sp, rows, x)
+    scale = np.sqrt(np.mean(np.abs(y) ** 2))
+    err = np.abs(y[rows] - z).max() / scale
+    assert err <= 10 * eps, err
+
+
+@pytest.mark.parametrize("fam,eq,op,k", [("p0", "laplace", "slp", 0.0),
+                                         ("p0", "helmholtz", "slp", 4.0),
+                                         ("p1c", "laplace", "dlp", 0.0)])
+def test_device_matvec_equals_host_matvec(fam, eq, op, k):
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix, hmat_matvec
+    v, e, spec, sp, bt = problem(12, fam, eq, op, k)
+    h = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=1e-5))
+    x = np.random.default_rng(7).standard_normal(sp.n_dofs)
+    yd = hmat_matvec(h, x, device=True)
+    yh = hmat_matvec(h, x, device=False)
+    assert np.abs(yd - yh).max() <= 1e-12 * np.abs(yh).max()
+
+
+def test_execute_is_bitwise_deterministic():
+    from paper_1711_01897_b200.backend import init_gpu_device
+    from paper_1711_01897_b200.discretization import make_integration_context
+    from paper_1711_01897_b200.hmatrix import AcaConfig, AssemblyConfig, _assemble_part
+    v, e, spec, sp, bt = problem(40, "p0", "laplace", "slp", 0.0)
+    dev = init_gpu_device(make_integration_context(spec, sp, sp))
+    part = _assemble_part(dev, bt, np.arange(len(bt.leaf_array)), sp, sp,
+                          AcaConfig(epsilon=1e-3), AssemblyConfig())
+    a1 = [np.array(a, copy=True) for a in part.arenas()]
+    meta1 = (part.kind.copy(), part.rank.copy(), part.off_u.copy(), part.off_d.copy())
+    part.execute()
+    a2 = part.arenas()
+    assert all(np.array_equal(p, q) for p, q in zip(a1, a2))
+    assert all(np.array_equal(p, q) for p, q in
+               zip(meta1, (part.kind, part.rank, part.off_u, part.off_d)))
+    part.close()
+
+
+def test_single_precision_at_scale_vs_double():
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix
+    _, _, s64, sp, bt = problem(45, "p0", "laplace", "slp", 0.0)
+    _, _, s32, _, _ = problem(45, "p0", "laplace", "slp", 0.0, "single")
+    x = np.random.default_rng(3).standard_normal(sp.n_dofs)
+    y64 = assemble_hmatrix(s64, sp, sp, bt, AcaConfig(epsilon=1e-4)).matvec(x)
+    y32 = assemble_hmatrix(s32, sp, sp, bt, AcaConfig(epsilon=1e-4)).matvec(x)
+    assert np.linalg.norm(y32 - y64) <= 5e-4 * np.linalg.norm(y64)
+
+
+def test_hull_mesh_assembly_vs_exact_rows():
+    """Elongated hull (C4 geometry class): Helmholtz SLP P0 rows."""
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix
+    from paper_1711_01897_b200.meshes import elongated_hull
+    v, e = elongated_hull(48, 160)
+    _, _, spec, sp, bt = problem((v, e), "p0", "helmholtz", "slp", 6.0)
+    eps = 1e-4
+    h = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=eps))
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(sp.n_dofs)
+    y = h.matvec(x)
+    rows = rng.choice(sp.n_dofs, size=6, replace=False)
+    z = exact_rows(spec, sp, rows, x)
+    assert np.abs(y[rows] - z).max() <= 10 * eps * np.sqrt(np.mean(np.abs(y) ** 2))
