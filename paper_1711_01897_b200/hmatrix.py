@@ -158,9 +158,12 @@ def pinned_empty(n: int, dtype) -> np.ndarray:
 class _DevicePart:
     """One hbem_hmat (one GPU's share of the leaves) and its host arenas."""
 
-    def __init__(self, handle, n_leaves, shapes, dtype, n_rows=0):
+    def __init__(self, handle, n_leaves, shapes, dtype, n_rows=0, context=None):
         self.handle = handle
         self.n_rows = n_rows
+        # the device context (geometry, rules) must outlive the handle: the
+        # assembler reads it on re-execute and matvec reads its precision
+        self.context = context
         self.dtype = dtype
         self.shapes = shapes  # (L, 2) h, w
         self.n_leaves = n_leaves
@@ -235,6 +238,7 @@ class _DevicePart:
             lib.hbem_hmat_destroy(self.handle)
             self.handle = None
         self._arenas = None
+        self.context = None
 
     def __del__(self):
         try:
@@ -391,7 +395,8 @@ def _assemble_part(dev_ctx, tree: BlockClusterTree, leaf_ids, test_space, trial_
     h = C.c_void_p()
     check(lib.hbem_hmat_assemble(dev_ctx.handle, C.byref(d), stream, C.byref(h)))
     shapes = np.stack([rn[la[:, 0], 1] - rn[la[:, 0], 0], cn[la[:, 1], 1] - cn[la[:, 1], 0]], 1)
-    return _DevicePart(h, len(la), shapes, dev_ctx.spec.result_dtype, n_rows=len(rp))
+    return _DevicePart(h, len(la), shapes, dev_ctx.spec.result_dtype, n_rows=len(rp),
+                       context=dev_ctx)
 
 
 COUNTER_NAMES = ("host_jobs", "backend_jobs", "singular_pairs", "aca_converged", "aca_exhausted",
