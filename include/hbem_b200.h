@@ -173,6 +173,13 @@ typedef struct hbem_hmat_desc {
   int64_t k_max;                    /* <= 0 means None (min(m, n)) */
   int32_t rank_capacity;            /* initial per-block factor capacity, 0 = auto */
   int32_t pointers_on_device;       /* 1: all arrays above are device pointers */
+  /* optional host output arenas (page-locked, e.g. hbem_host_alloc), element
+     units of the result dtype; when set, execute streams the low-rank
+     factors of every wave and the dense leaves into them while the
+     assembly runs (hbem_hmat_copy_arenas is then not needed).  A capacity
+     smaller than the payload is a CapacityError. */
+  void *out_u, *out_v, *out_dense;
+  int64_t out_u_cap, out_v_cap, out_dense_cap;
 } hbem_hmat_desc;
 
 /* counters returned by hbem_hmat_stats (names as _LeafAssembler.counters,

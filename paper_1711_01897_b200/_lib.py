@@ -80,6 +80,12 @@ class HmatDesc(C.Structure):
         ("k_max", C.c_int64),
         ("rank_capacity", C.c_int32),
         ("pointers_on_device", C.c_int32),
+        ("out_u", C.c_void_p),
+        ("out_v", C.c_void_p),
+        ("out_dense", C.c_void_p),
+        ("out_u_cap", C.c_int64),
+        ("out_v_cap", C.c_int64),
+        ("out_dense_cap", C.c_int64),
     ]
 
 

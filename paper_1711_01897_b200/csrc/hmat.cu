@@ -35,6 +35,8 @@
 #include <numeric>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "hmat_common.cuh"
 
 namespace hb {
@@ -119,11 +121,13 @@ __global__ void k_expand(const int *slots, int n, AcaDev S, const long long *off
   }
 }
 
-// pack the factors of low-rank blocks [first, last) into U/V staging
+// pack the factors of low-rank blocks into the U / V arenas, one CTA per
+// block (v = r / p as r * (1 / p): one division per term)
 template <typename Tr, bool Cc, typename V = typename Num<Tr, Cc>::V>
 __global__ void k_pack_factors(const int *slots, int n, AcaDev S, const long long *uoff,
                                const long long *voff, long long ubase, long long vbase, V *u,
                                V *v) {
+  using N = Num<Tr, Cc>;
   const int q = blockIdx.x;
   if (q >= n) return;
   const int b = slots[q];
@@ -133,13 +137,56 @@ __global__ void k_pack_factors(const int *slots, int n, AcaDev S, const long lon
     const V *t = pool + S.terms[(long long)b * S.tmax + l];
     for (int r = threadIdx.x; r < h; r += blockDim.x)
       u[uoff[q] - ubase + (long long)l * h + r] = t[r];
+    const V inv = N::div(N::mk(Tr(1), Tr(0)), t[h + w]);
     for (int c = threadIdx.x; c < w; c += blockDim.x)
-      v[voff[q] - vbase + (long long)l * w + c] = Num<Tr, Cc>::div(t[h + c], t[h + w]);
+      v[voff[q] - vbase + (long long)l * w + c] = N::fma_acc(N::zero(), t[h + c], inv);
   }
 }
 
-}  // namespace hb
+// per-wave emission of converged low-rank blocks (lowrank_leaf rule,
+// hmatrix.py:721-729): flags in block order, not yet emitted
+__global__ void k_emit_flags(AcaDev S, int na, unsigned char *emitted, unsigned char *flag) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= na) return;
+  const long long h = S.h[b], w = S.w[b], k = S.rank[b];
+  const bool f = !emitted[b] && S.status[b] == ST_CONVERGED && k * (h + w) < h * w;
+  flag[b] = f ? 1 : 0;
+  if (f) emitted[b] = 1;
+}
 
+__global__ void k_emit_need(AcaDev S, const int *list, const int *cnt, int na, longlong2 *need) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= na) return;
+  longlong2 d = make_longlong2(0, 0);
+  if (p < *cnt) {
+    const int b = list[p];
+    const long long k = S.rank[b];
+    d = make_longlong2((long long)S.h[b] * k, (long long)S.w[b] * k);
+  }
+  need[p] = d;
+}
+
+__global__ void k_emit_offsets(const int *list, int n, const longlong2 *scan,
+                               const longlong2 *need, long long ubase, long long vbase,
+                               long long *blk_uoff, long long *blk_voff, long long *q_uoff,
+                               long long *q_voff) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int b = list[p];
+  const long long uo = ubase + scan[p].x - need[p].x, vo = vbase + scan[p].y - need[p].y;
+  blk_uoff[b] = uo;
+  blk_voff[b] = vo;
+  q_uoff[p] = uo;
+  q_voff[p] = vo;
+}
+
+struct SumLL2 {
+  __device__ __forceinline__ longlong2 operator()(const longlong2 &a, const longlong2 &b) const {
+    return make_longlong2(a.x + b.x, a.y + b.y);
+  }
+};
+
+}  // namespace hb
 
 using namespace hb;
 
@@ -299,6 +346,23 @@ struct hbem_hmat {
   int *mv_lr = nullptr, *mv_ad = nullptr;
   long long *mv_ad_l = nullptr;
   std::vector<int64_t> lr_uoff, lr_voff;
+  // streamed payloads: per-wave packing of converged low-rank blocks into
+  // device U / V arenas (growable), optional D2H into caller host arenas
+  VPool uarena, varena;
+  unsigned char *emitted = nullptr, *emit_flag = nullptr;
+  int *emit_list = nullptr, *emit_cnt = nullptr;
+  longlong2 *emit_need = nullptr, *emit_scan = nullptr;
+  long long *blk_uoff = nullptr, *blk_voff = nullptr, *q_uoff = nullptr, *q_voff = nullptr;
+  void *emit_tmp = nullptr;
+  size_t emit_tmp_bytes = 0;
+  long long u_top = 0, v_top = 0;
+  bool packed = false;  // U / V arenas hold the current factors
+  bool streaming() const { return out_u || out_v || out_dense; }
+  void *out_u = nullptr, *out_v = nullptr, *out_dense = nullptr;
+  long long out_u_cap = 0, out_v_cap = 0, out_dense_cap = 0;
+  cudaStream_t cp = nullptr;    // factor packing + D2H, middle priority
+  cudaStream_t cpd = nullptr;   // dense-arena D2H (waits for the near field)
+  cudaEvent_t emit_ev = nullptr;
   cudaStream_t side = nullptr;  // near-field leaves, lowest priority
   cudaStream_t hi = nullptr;    // ACA waves, highest priority
   cudaEvent_t side_done = nullptr;
@@ -306,11 +370,13 @@ struct hbem_hmat {
   cudaEvent_t iev[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // integration launches
   bool int_pending[2] = {false, false};
   std::vector<void *> dev_allocs;
+  std::vector<void *> exec_allocs;  // per-execute scratch
   hbem_hmat_stats stats{};
   double setup_s = 0.0;
   ~hbem_hmat() {
     cudaSetDevice(device);
     for (void *p : dev_allocs) cudaFree(p);
+    for (void *p : exec_allocs) cudaFree(p);
     cudaFree(dense_nf);
     cudaFree(dense_adm);
     cudaFree(partA);
@@ -322,6 +388,9 @@ struct hbem_hmat {
     if (mail) cudaFreeHost(mail);
     if (side) cudaStreamDestroy(side);
     if (hi) cudaStreamDestroy(hi);
+    if (cp) cudaStreamDestroy(cp);
+    if (cpd) cudaStreamDestroy(cpd);
+    if (emit_ev) cudaEventDestroy(emit_ev);
     if (side_done) cudaEventDestroy(side_done);
     for (auto e : ev)
       if (e) cudaEventDestroy(e);
@@ -348,6 +417,25 @@ template <typename X> int dalloc(hbem_hmat *H, X **p, size_t n) {
   }
   H->dev_allocs.push_back(q);
   *p = static_cast<X *>(q);
+  return HBEM_OK;
+}
+
+// per-execute scratch: released at the start of the next execute / destroy
+template <typename X> int dalloc_tmp(hbem_hmat *H, X **p, size_t n) {
+  void *q = nullptr;
+  cudaError_t e = cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(X));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(HBEM_ERR_CAPACITY, "device allocation of %zu bytes failed: %s",
+                     n * sizeof(X), cudaGetErrorString(e));
+  }
+  H->exec_allocs.push_back(q);
+  *p = static_cast<X *>(q);
+  return HBEM_OK;
+}
+template <typename X> int upload_tmp(hbem_hmat *H, X **p, const std::vector<X> &v) {
+  HB_CHECK(dalloc_tmp(H, p, v.size()));
+  if (!v.empty()) HB_CUDA(cudaMemcpy(*p, v.data(), v.size() * sizeof(X), cudaMemcpyHostToDevice));
   return HBEM_OK;
 }
 
@@ -677,7 +765,42 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
     HB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     HB_CUDA(cudaStreamCreateWithPriority(&H->side, cudaStreamNonBlocking, least));
     HB_CUDA(cudaStreamCreateWithPriority(&H->hi, cudaStreamNonBlocking, greatest));
+    // payload packing between the two: ahead of the near field so the PCIe
+    // copies start while the ACA waves still run
+    HB_CUDA(cudaStreamCreateWithPriority(&H->cp, cudaStreamNonBlocking,
+                                         greatest < least ? greatest + 1 : least));
+    HB_CUDA(cudaStreamCreateWithPriority(&H->cpd, cudaStreamNonBlocking, least));
+    HB_CUDA(cudaEventCreateWithFlags(&H->emit_ev, cudaEventDisableTiming));
   }
+  // streamed payload arenas (virtual ranges, mapped as blocks converge)
+  HB_CHECK(H->uarena.init(H->device, std::max<size_t>(free_b / 2, (size_t)4 << 30)));
+  HB_CHECK(H->varena.init(H->device, std::max<size_t>(free_b / 2, (size_t)4 << 30)));
+  HB_CHECK(dalloc(H, &H->emitted, std::max(na, 1)));
+  HB_CHECK(dalloc(H, &H->emit_flag, std::max(na, 1)));
+  HB_CHECK(dalloc(H, &H->emit_list, std::max(na, 1)));
+  HB_CHECK(dalloc(H, &H->emit_cnt, 1));
+  HB_CHECK(dalloc(H, &H->emit_need, std::max(na, 1)));
+  HB_CHECK(dalloc(H, &H->emit_scan, std::max(na, 1)));
+  HB_CHECK(dalloc(H, &H->blk_uoff, std::max(na, 1)));
+  HB_CHECK(dalloc(H, &H->blk_voff, std::max(na, 1)));
+  HB_CHECK(dalloc(H, &H->q_uoff, std::max(na, 1)));
+  HB_CHECK(dalloc(H, &H->q_voff, std::max(na, 1)));
+  {
+    size_t b1 = 0, b2 = 0;
+    cub::DeviceSelect::Flagged(nullptr, b1, cub::CountingInputIterator<int>(0),
+                               (const unsigned char *)nullptr, (int *)nullptr, (int *)nullptr,
+                               std::max(na, 1));
+    cub::DeviceScan::InclusiveScan(nullptr, b2, (const longlong2 *)nullptr, (longlong2 *)nullptr,
+                                   SumLL2(), std::max(na, 1));
+    H->emit_tmp_bytes = std::max(b1, b2);
+    HB_CHECK(dalloc(H, (char **)&H->emit_tmp, H->emit_tmp_bytes));
+  }
+  H->out_u = d->out_u;
+  H->out_v = d->out_v;
+  H->out_dense = d->out_dense;
+  H->out_u_cap = d->out_u_cap;
+  H->out_v_cap = d->out_v_cap;
+  H->out_dense_cap = d->out_dense_cap;
   HB_CUDA(cudaEventCreateWithFlags(&H->side_done, cudaEventDisableTiming));
   for (auto &e : H->ev) HB_CUDA(cudaEventCreate(&e));
   for (auto &pr : H->iev)
@@ -735,6 +858,73 @@ int run_phase(hbem_hmat *H, const Prob<T> &P, int col, long long &pool_top, int 
   return aca_phase<T, C>(P, S, A, ctx->op, ctx->helm, H->nt, H->ns, n, tot.items, st);
 }
 
+// pack the low-rank blocks converged since the last call into the device
+// U / V arenas (cp stream, low priority) and stream them into the caller's
+// host arenas when given; one host read per call
+template <typename T, bool C> int emit_converged(hbem_hmat *H, cudaStream_t st, bool pack = true) {
+  using V = typename Num<T, C>::V;
+  const int na = H->na;
+  if (na <= 0) return HBEM_OK;
+  AcaDev &S = H->S;
+  k_emit_flags<<<(na + 255) / 256, 256, 0, st>>>(S, na, H->emitted, H->emit_flag);
+  size_t tb = H->emit_tmp_bytes;
+  HB_CUDA(cub::DeviceSelect::Flagged(H->emit_tmp, tb, cub::CountingInputIterator<int>(0),
+                                     H->emit_flag, H->emit_list, H->emit_cnt, na, st));
+  k_emit_need<<<(na + 255) / 256, 256, 0, st>>>(S, H->emit_list, H->emit_cnt, na, H->emit_need);
+  tb = H->emit_tmp_bytes;
+  HB_CUDA(cub::DeviceScan::InclusiveScan(H->emit_tmp, tb, H->emit_need, H->emit_scan, SumLL2(),
+                                         na, st));
+  HB_CUDA(cudaMemcpyAsync(&H->mail->tot, H->emit_scan + (na - 1), sizeof(longlong2),
+                          cudaMemcpyDeviceToHost, st));
+  HB_CUDA(cudaMemcpyAsync(&H->mail->n, H->emit_cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
+  HB_CUDA(cudaStreamSynchronize(st));
+  const int n = H->mail->n;
+  const longlong2 tot = *reinterpret_cast<const longlong2 *>(&H->mail->tot);
+  if (n == 0) return HBEM_OK;
+  const size_t vb = sizeof(V);
+  if (pack) {
+    HB_CHECK(H->uarena.grow((size_t)(H->u_top + tot.x) * vb));
+    HB_CHECK(H->varena.grow((size_t)(H->v_top + tot.y) * vb));
+  }
+  if (H->out_u && H->u_top + tot.x > H->out_u_cap)
+    return set_error(HBEM_ERR_CAPACITY, "host U arena of %lld values too small",
+                     (long long)H->out_u_cap);
+  if (H->out_v && H->v_top + tot.y > H->out_v_cap)
+    return set_error(HBEM_ERR_CAPACITY, "host V arena of %lld values too small",
+                     (long long)H->out_v_cap);
+  k_emit_offsets<<<(n + 255) / 256, 256, 0, st>>>(H->emit_list, n, H->emit_scan, H->emit_need,
+                                                  H->u_top, H->v_top, H->blk_uoff, H->blk_voff,
+                                                  H->q_uoff, H->q_voff);
+  if (!pack) {
+    H->u_top += tot.x;
+    H->v_top += tot.y;
+    return HBEM_OK;
+  }
+  HB_CUDA(cudaEventRecord(H->emit_ev, st));
+  HB_CUDA(cudaStreamWaitEvent(H->cp, H->emit_ev, 0));
+  // the emission list is rebuilt next wave: the pack reads a private copy
+  int *lst = nullptr;
+  long long *uo = nullptr, *vo = nullptr;
+  HB_CHECK(dalloc_tmp(H, &lst, (size_t)n));
+  HB_CHECK(dalloc_tmp(H, &uo, (size_t)n));
+  HB_CHECK(dalloc_tmp(H, &vo, (size_t)n));
+  HB_CUDA(cudaMemcpyAsync(lst, H->emit_list, (size_t)n * 4, cudaMemcpyDeviceToDevice, H->cp));
+  HB_CUDA(cudaMemcpyAsync(uo, H->q_uoff, (size_t)n * 8, cudaMemcpyDeviceToDevice, H->cp));
+  HB_CUDA(cudaMemcpyAsync(vo, H->q_voff, (size_t)n * 8, cudaMemcpyDeviceToDevice, H->cp));
+  V *ua = reinterpret_cast<V *>(H->uarena.base), *va = reinterpret_cast<V *>(H->varena.base);
+  k_pack_factors<T, C><<<n, 128, 0, H->cp>>>(lst, n, S, uo, vo, 0, 0, ua, va);
+  HB_CUDA(cudaGetLastError());
+  if (H->out_u)
+    HB_CUDA(cudaMemcpyAsync(static_cast<V *>(H->out_u) + H->u_top, ua + H->u_top,
+                            (size_t)tot.x * vb, cudaMemcpyDeviceToHost, H->cp));
+  if (H->out_v)
+    HB_CUDA(cudaMemcpyAsync(static_cast<V *>(H->out_v) + H->v_top, va + H->v_top,
+                            (size_t)tot.y * vb, cudaMemcpyDeviceToHost, H->cp));
+  H->u_top += tot.x;
+  H->v_top += tot.y;
+  return HBEM_OK;
+}
+
 template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   using V = typename Num<T, C>::V;
   hbem_ctx *ctx = H->ctx;
@@ -747,6 +937,14 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   hbem_hmat_stats &ST = H->stats;
   const hbem_hmat_stats zero{};
   ST = zero;
+  for (void *p : H->exec_allocs) cudaFree(p);
+  H->exec_allocs.clear();
+  H->u_top = H->v_top = 0;
+  if (na > 0) {
+    HB_CUDA(cudaMemsetAsync(H->emitted, 0, na, st));
+    HB_CUDA(cudaMemsetAsync(H->blk_uoff, 0xff, (size_t)na * 8, st));
+    HB_CUDA(cudaMemsetAsync(H->blk_voff, 0xff, (size_t)na * 8, st));
+  }
   // ---- tree-ordered element records (P0) -------------------------------------------
   if (H->p0) {
     HB_CHECK(build_recs<T>(P.g, ctx->elem, H->rperm, H->n_rows, static_cast<T *>(H->trec), st));
@@ -790,6 +988,14 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   }
   HB_CUDA(cudaEventRecord(H->side_done, H->side));
   HB_CUDA(cudaEventRecord(H->ev[3], H->side));
+  if (H->out_dense && H->nf_entries > 0) {
+    if (H->nf_entries > H->out_dense_cap)
+      return set_error(HBEM_ERR_CAPACITY, "host dense arena of %lld values too small",
+                       (long long)H->out_dense_cap);
+    HB_CUDA(cudaStreamWaitEvent(H->cpd, H->side_done, 0));
+    HB_CUDA(cudaMemcpyAsync(H->out_dense, H->dense_nf, (size_t)H->nf_entries * sizeof(V),
+                            cudaMemcpyDeviceToHost, H->cpd));
+  }
   // ---- ACA waves ------------------------------------------------------------------
   HB_CUDA(cudaMemsetAsync(S.stat, 0, 32, st));
   int waves = 0;
@@ -803,7 +1009,8 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
       HB_CHECK((run_phase<T, C>(H, P, 0, pool_top, waves, &nA, st)));
       if (nA == 0) break;
       HB_CHECK((run_phase<T, C>(H, P, 1, pool_top, waves, &nC, st)));
-      launches += nC > 0 ? 10 : 7;
+      if (H->streaming()) HB_CHECK((emit_converged<T, C>(H, st)));
+      launches += (nC > 0 ? 10 : 7) + (H->streaming() ? 4 : 0);
       HB_CUDA(cudaEventRecord(H->ev[1], st));
       HB_CUDA(cudaEventSynchronize(H->ev[1]));
       float ms = 0.f;
@@ -822,11 +1029,20 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
       ++waves;
     }
   }
+  if (!H->streaming() && na > 0) {
+    // offsets of every low-rank block (block order); packing deferred to
+    // hbem_hmat_copy_arenas (the device-resident H-matrix is the pool)
+    HB_CHECK((emit_converged<T, C>(H, st, /*pack=*/false)));
+  }
+  H->packed = H->streaming();
   const auto t_aca = clk::now();
   // ---- classify admissible blocks (lowrank_leaf, hmatrix.py:721-735) -------------
   std::vector<int> st_h(na), rk_h(na), ex_h(na);
   std::vector<double> rs_h(na);
+  std::vector<long long> bu_h(na), bv_h(na);
   if (na > 0) {
+    HB_CUDA(cudaMemcpy(bu_h.data(), H->blk_uoff, (size_t)na * 8, cudaMemcpyDeviceToHost));
+    HB_CUDA(cudaMemcpy(bv_h.data(), H->blk_voff, (size_t)na * 8, cudaMemcpyDeviceToHost));
     HB_CUDA(cudaMemcpy(st_h.data(), S.status, na * 4, cudaMemcpyDeviceToHost));
     HB_CUDA(cudaMemcpy(rk_h.data(), S.rank, na * 4, cudaMemcpyDeviceToHost));
     HB_CUDA(cudaMemcpy(ex_h.data(), S.exhausted, na * 4, cudaMemcpyDeviceToHost));
@@ -858,14 +1074,13 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
     if (s == ST_CONVERGED) {
       ST.aca_converged++;
       if ((long long)rk_h[q] * (h + w) < hw) {
+        // packed by emit_converged in the wave it converged
         H->kind[lf] = 1;
         H->lowrank_slots.push_back(q);
-        H->off_u[lf] = H->u_entries;
-        H->off_v[lf] = H->v_entries;
-        H->lr_uoff.push_back(H->u_entries);
-        H->lr_voff.push_back(H->v_entries);
-        H->u_entries += (long long)h * rk_h[q];
-        H->v_entries += (long long)w * rk_h[q];
+        H->off_u[lf] = bu_h[q];
+        H->off_v[lf] = bv_h[q];
+        H->lr_uoff.push_back(bu_h[q]);
+        H->lr_voff.push_back(bv_h[q]);
         ST.lowrank_leaves++;
         continue;
       }
@@ -880,6 +1095,8 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
     H->off_dense[lf] = H->nf_entries + adm_dense;
     adm_dense += hw;
   }
+  H->u_entries = H->u_top;
+  H->v_entries = H->v_top;
   ST.dense_leaves = H->nd + (int64_t)expand_slots.size() + (int64_t)fb_r0.size();
   H->ad_r0.clear(); H->ad_c0.clear(); H->ad_h.clear(); H->ad_w.clear();
   H->ad_off.clear(); H->ad_rowbase.clear();
@@ -908,8 +1125,8 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   if (!expand_slots.empty()) {
     int *slots;
     long long *offs;
-    HB_CHECK(upload(H, &slots, expand_slots));
-    HB_CHECK(upload(H, &offs, expand_off));
+    HB_CHECK(upload_tmp(H, &slots, expand_slots));
+    HB_CHECK(upload_tmp(H, &offs, expand_off));
     k_expand<T, C><<<(unsigned)expand_slots.size(), 128, 0, st>>>(
         slots, (int)expand_slots.size(), S, offs, H->dense_adm);
     HB_CUDA(cudaGetLastError());
@@ -932,21 +1149,21 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
     }
     int *p;
     long long *pl;
-    HB_CHECK(upload(H, &p, tslot)); F.tile_slot = p;
-    HB_CHECK(upload(H, &p, tstart)); F.tile_start = p;
-    HB_CHECK(upload(H, &p, fb_r0)); F.r0 = p;
-    HB_CHECK(upload(H, &p, fb_c0)); F.c0 = p;
-    HB_CHECK(upload(H, &p, fb_h)); F.h = p;
-    HB_CHECK(upload(H, &p, fb_w)); F.w = p;
-    HB_CHECK(upload(H, &pl, fb_off)); F.off = pl;
+    HB_CHECK(upload_tmp(H, &p, tslot)); F.tile_slot = p;
+    HB_CHECK(upload_tmp(H, &p, tstart)); F.tile_start = p;
+    HB_CHECK(upload_tmp(H, &p, fb_r0)); F.r0 = p;
+    HB_CHECK(upload_tmp(H, &p, fb_c0)); F.c0 = p;
+    HB_CHECK(upload_tmp(H, &p, fb_h)); F.h = p;
+    HB_CHECK(upload_tmp(H, &p, fb_w)); F.w = p;
+    HB_CHECK(upload_tmp(H, &pl, fb_off)); F.off = pl;
     F.out = H->dense_adm;
-    HB_CHECK(dalloc(H, &F.sing_count, 1));
-    HB_CHECK(dalloc(H, &F.stat, 2));
+    HB_CHECK(dalloc_tmp(H, &F.sing_count, 1));
+    HB_CHECK(dalloc_tmp(H, &F.stat, 2));
     HB_CUDA(cudaMemsetAsync(F.sing_count, 0, 8, st));
     HB_CUDA(cudaMemsetAsync(F.stat, 0, 16, st));
     if (nt == 1 && ns == 1) {
-      HB_CHECK(dalloc(H, &F.sing_slot, ent));
-      HB_CHECK(dalloc(H, &F.sing_pos, ent));
+      HB_CHECK(dalloc_tmp(H, &F.sing_slot, ent));
+      HB_CHECK(dalloc_tmp(H, &F.sing_pos, ent));
     }
     const unsigned ntl = (unsigned)tslot.size();
     int rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc,
@@ -975,6 +1192,17 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
     fb_sing += fs[1];
     ST.regular_pairs += ent;
   }
+  if (H->out_dense && adm_dense > 0) {
+    if (H->nf_entries + adm_dense > H->out_dense_cap)
+      return set_error(HBEM_ERR_CAPACITY, "host dense arena of %lld values too small",
+                       (long long)H->out_dense_cap);
+    HB_CUDA(cudaEventRecord(H->emit_ev, st));
+    HB_CUDA(cudaStreamWaitEvent(H->cpd, H->emit_ev, 0));
+    HB_CUDA(cudaMemcpyAsync(static_cast<V *>(H->out_dense) + H->nf_entries, H->dense_adm,
+                            (size_t)adm_dense * sizeof(V), cudaMemcpyDeviceToHost, H->cpd));
+  }
+  HB_CUDA(cudaStreamSynchronize(H->cp));
+  HB_CUDA(cudaStreamSynchronize(H->cpd));
   HB_CUDA(cudaStreamWaitEvent(st, H->side_done, 0));
   unsigned long long nf_sing = 0, nf_stat[2] = {0, 0}, aca_stat[2] = {0, 0};
   HB_CUDA(cudaMemcpyAsync(&nf_sing, H->D.sing_count, 8, cudaMemcpyDeviceToHost, st));
@@ -1134,19 +1362,12 @@ int hbem_hmat_copy_arenas(const hbem_hmat *hc, void *u, void *v, void *dense) {
                           (size_t)adm * vb, cudaMemcpyDeviceToHost, sd);
     if (e != cudaSuccess) return fail(e);
   }
-  if ((u || v) && !h->lowrank_slots.empty()) {
+  // low-rank factors: packed per wave when streaming, else packed here
+  if (!h->packed && !h->lowrank_slots.empty()) {
     const size_t n = h->lowrank_slots.size();
-    const long long chunk_vals = 32ll << 20;
     int *d_slots = nullptr;
     long long *d_uo = nullptr, *d_vo = nullptr;
-    void *su[2] = {nullptr, nullptr}, *sv[2] = {nullptr, nullptr};
-    long long cap[2] = {chunk_vals, chunk_vals};
-    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
-      e = cudaMalloc(&su[b], chunk_vals * vb);
-      if (e == cudaSuccess) { tmp.push_back(su[b]); e = cudaMalloc(&sv[b], chunk_vals * vb); }
-      if (e == cudaSuccess) tmp.push_back(sv[b]);
-    }
-    if (e == cudaSuccess) e = cudaMalloc(&d_slots, n * 4);
+    e = cudaMalloc(&d_slots, n * 4);
     if (e == cudaSuccess) { tmp.push_back(d_slots); e = cudaMalloc(&d_uo, n * 8); }
     if (e == cudaSuccess) { tmp.push_back(d_uo); e = cudaMalloc(&d_vo, n * 8); }
     if (e == cudaSuccess) tmp.push_back(d_vo);
@@ -1155,56 +1376,37 @@ int hbem_hmat_copy_arenas(const hbem_hmat *hc, void *u, void *v, void *dense) {
     if (e == cudaSuccess) e = cudaMemcpy(d_uo, h->lr_uoff.data(), n * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d_vo, h->lr_voff.data(), n * 8, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return fail(e);
-    size_t q0 = 0;
-    int buf = 0;
-    while (q0 < n) {
-      const long long ub = h->lr_uoff[q0], vbase = h->lr_voff[q0];
-      size_t q1 = q0 + 1;
-      while (q1 < n && (q1 + 1 < n ? h->lr_uoff[q1 + 1] : h->u_entries) - ub <= chunk_vals &&
-             (q1 + 1 < n ? h->lr_voff[q1 + 1] : h->v_entries) - vbase <= chunk_vals)
-        ++q1;
-      const long long ue = q1 < n ? h->lr_uoff[q1] : h->u_entries;
-      const long long ve = q1 < n ? h->lr_voff[q1] : h->v_entries;
-      cudaStream_t st = sp[buf];
-      const long long need = std::max(ue - ub, ve - vbase);
-      if (need > cap[buf]) {  // one oversized block: private staging
-        e = cudaStreamSynchronize(st);
-        if (e == cudaSuccess) e = cudaMalloc(&su[buf], need * vb);
-        if (e == cudaSuccess) { tmp.push_back(su[buf]); e = cudaMalloc(&sv[buf], need * vb); }
-        if (e == cudaSuccess) { tmp.push_back(sv[buf]); cap[buf] = need; }
-        if (e != cudaSuccess) return fail(e);
-      }
-      const int cnt = (int)(q1 - q0);
-      if (h->vbytes == 16)
-        k_pack_factors<double, true><<<cnt, 128, 0, st>>>(d_slots + q0, cnt, h->S, d_uo + q0,
-                                                          d_vo + q0, ub, vbase,
-                                                          (Cx<double> *)su[buf],
-                                                          (Cx<double> *)sv[buf]);
-      else if (h->vbytes == 8 && h->complex_)
-        k_pack_factors<float, true><<<cnt, 128, 0, st>>>(d_slots + q0, cnt, h->S, d_uo + q0,
-                                                         d_vo + q0, ub, vbase,
-                                                         (Cx<float> *)su[buf],
-                                                         (Cx<float> *)sv[buf]);
-      else if (h->vbytes == 8)
-        k_pack_factors<double, false><<<cnt, 128, 0, st>>>(d_slots + q0, cnt, h->S, d_uo + q0,
-                                                           d_vo + q0, ub, vbase,
-                                                           (double *)su[buf], (double *)sv[buf]);
-      else
-        k_pack_factors<float, false><<<cnt, 128, 0, st>>>(d_slots + q0, cnt, h->S, d_uo + q0,
-                                                          d_vo + q0, ub, vbase, (float *)su[buf],
-                                                          (float *)sv[buf]);
-      e = cudaGetLastError();
-      if (e == cudaSuccess && u)
-        e = cudaMemcpyAsync((char *)u + ub * vb, su[buf], (ue - ub) * vb, cudaMemcpyDeviceToHost,
-                            st);
-      if (e == cudaSuccess && v)
-        e = cudaMemcpyAsync((char *)v + vbase * vb, sv[buf], (ve - vbase) * vb,
-                            cudaMemcpyDeviceToHost, st);
-      if (e != cudaSuccess) return fail(e);
-      q0 = q1;
-      buf ^= 1;
+    if (h->uarena.grow((size_t)h->u_entries * vb) != HBEM_OK ||
+        h->varena.grow((size_t)h->v_entries * vb) != HBEM_OK) {
+      done();
+      return HBEM_ERR_CAPACITY;
     }
+    const int cnt = (int)n;
+    void *ua = reinterpret_cast<void *>(h->uarena.base), *va = reinterpret_cast<void *>(h->varena.base);
+    if (h->vbytes == 16)
+      k_pack_factors<double, true><<<cnt, 128, 0, sp[0]>>>(d_slots, cnt, h->S, d_uo, d_vo, 0, 0,
+                                                           (Cx<double> *)ua, (Cx<double> *)va);
+    else if (h->vbytes == 8 && h->complex_)
+      k_pack_factors<float, true><<<cnt, 128, 0, sp[0]>>>(d_slots, cnt, h->S, d_uo, d_vo, 0, 0,
+                                                          (Cx<float> *)ua, (Cx<float> *)va);
+    else if (h->vbytes == 8)
+      k_pack_factors<double, false><<<cnt, 128, 0, sp[0]>>>(d_slots, cnt, h->S, d_uo, d_vo, 0, 0,
+                                                            (double *)ua, (double *)va);
+    else
+      k_pack_factors<float, false><<<cnt, 128, 0, sp[0]>>>(d_slots, cnt, h->S, d_uo, d_vo, 0, 0,
+                                                           (float *)ua, (float *)va);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(sp[0]);
+    if (e != cudaSuccess) return fail(e);
+    h->packed = true;
   }
+  if (e == cudaSuccess && u && h->u_entries > 0)
+    e = cudaMemcpyAsync(u, reinterpret_cast<const void *>(h->uarena.base),
+                        (size_t)h->u_entries * vb, cudaMemcpyDeviceToHost, sp[0]);
+  if (e == cudaSuccess && v && h->v_entries > 0)
+    e = cudaMemcpyAsync(v, reinterpret_cast<const void *>(h->varena.base),
+                        (size_t)h->v_entries * vb, cudaMemcpyDeviceToHost, sp[1]);
+  if (e != cudaSuccess) return fail(e);
   done();
   HB_CUDA(cudaGetLastError());
   return HBEM_OK;

@@ -192,9 +192,13 @@ class _DevicePart:
 
     def execute(self, stream=None):
         """Re-run the whole assembly on the device (inputs already resident);
-        deterministic, so the payloads are unchanged."""
+        deterministic, so the payloads are unchanged (and re-streamed into the
+        host output arenas if the part was assembled with ``out``)."""
+        arenas = self._arenas if getattr(self, "_streamed", False) else None
         check(lib.hbem_hmat_execute(self.handle, stream))
         self._refresh()
+        if arenas is not None:
+            self._arenas = arenas
 
     def _host_array(self, n, pinned):
         return pinned_empty(n, self.dtype) if pinned else np.empty(n, self.dtype)
@@ -369,7 +373,10 @@ def split_leaves(tree: BlockClusterTree, parts: int) -> list[np.ndarray]:
 
 
 def _assemble_part(dev_ctx, tree: BlockClusterTree, leaf_ids, test_space, trial_space,
-                   cfg: AcaConfig, acfg: AssemblyConfig, stream=None) -> _DevicePart:
+                   cfg: AcaConfig, acfg: AssemblyConfig, stream=None, out=None) -> _DevicePart:
+    """One GPU's share of the leaves.  ``out`` = (u, v, dense) page-locked host
+    arrays of the result dtype: the payloads are streamed into them while the
+    assembly runs (hbem_hmat_desc.out_*), wave by wave."""
     rows, cols = tree.rows, tree.cols
     la = np.ascontiguousarray(tree.leaf_array[leaf_ids])
     keep = [la]
@@ -392,11 +399,24 @@ def _assemble_part(dev_ctx, tree: BlockClusterTree, leaf_ids, test_space, trial_
     d.k_max = int(cfg.k_max) if cfg.k_max is not None else 0
     d.rank_capacity = int(acfg.rank_capacity)
     d.pointers_on_device = 0
+    if out is not None:
+        rd = np.dtype(dev_ctx.spec.result_dtype)
+        for a in out:
+            if a.dtype != rd:
+                raise ConfigError(f"output arenas must have dtype {rd}, got {a.dtype}")
+        d.out_u, d.out_v, d.out_dense = (_lib.vptr(a) for a in out)
+        d.out_u_cap, d.out_v_cap, d.out_dense_cap = (len(a) for a in out)
     h = C.c_void_p()
     check(lib.hbem_hmat_assemble(dev_ctx.handle, C.byref(d), stream, C.byref(h)))
     shapes = np.stack([rn[la[:, 0], 1] - rn[la[:, 0], 0], cn[la[:, 1], 1] - cn[la[:, 1], 0]], 1)
-    return _DevicePart(h, len(la), shapes, dev_ctx.spec.result_dtype, n_rows=len(rp),
+    part = _DevicePart(h, len(la), shapes, dev_ctx.spec.result_dtype, n_rows=len(rp),
                        context=dev_ctx)
+    if out is not None:
+        s = part.stats
+        part._arenas = (out[0][: s["u_entries"]], out[1][: s["v_entries"]],
+                        out[2][: s["dense_entries"]])
+        part._streamed = True
+    return part
 
 
 COUNTER_NAMES = ("host_jobs", "backend_jobs", "singular_pairs", "aca_converged", "aca_exhausted",
