@@ -30,6 +30,9 @@
 namespace hb {
 
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef HB_EXPERIMENT
+#define HB_EXPERIMENT 0  // timing experiments only (bit 1: no tile argmax, 2: no dots, 4: no residual)
+#endif
 
 // ---------------------------------------------------------------------------
 // state init, list selection, needs, jobs
@@ -247,7 +250,7 @@ __device__ __forceinline__ void aca_epi(const AcaDev &S, const JobS &J, const V_
   // f_l at this lane's entry: fb[l * 32 + lane] (valid lanes only)
 #pragma unroll
   for (int l = 0; l < kFinRegs; ++l)
-    if (l < kk && valid) val = N::fms(val, cs[l], fb[l * 32 + lane]);
+    if (!(HB_EXPERIMENT & 4) && l < kk && valid) val = N::fms(val, cs[l], fb[l * 32 + lane]);
   // terms beyond the register batch (late waves of high-rank blocks)
   const long long *tl = S.terms + (long long)J.b * S.tmax;
   const int fixo = COL ? J.h + J.fix : J.fix;
@@ -262,7 +265,9 @@ __device__ __forceinline__ void aca_epi(const AcaDev &S, const JobS &J, const V_
   double best = (valid && !masked) ? N::abs(val) : -1.0;
   int bidx = (valid && !masked) ? idx : 0x7fffffff;
   double ss = valid ? N::nrm(val) : 0.0;
+#if !(HB_EXPERIMENT & 1)
   warp_argmax_sum(best, bidx, ss);
+#endif
   double *rec = S.part + J.part + (long long)t * part_len(k, NC);
   if (lane == 0) {
     rec[0] = best;
@@ -270,7 +275,7 @@ __device__ __forceinline__ void aca_epi(const AcaDev &S, const JobS &J, const V_
     rec[2] = ss;
   }
   // dots vdot(f_l, val) of the register batch: transposed reduction
-  if (kk > 0) {
+  if (!(HB_EXPERIMENT & 2) && kk > 0) {
     double dr[8], di[8];
 #pragma unroll
     for (int l = 0; l < 8; ++l) {
@@ -420,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
             tm &= tm - 1;
             const int ev = __shfl_sync(kFull, my.ev.w, src);
             const double2 sv =
-                singular_warp<OP, HELM>(P.G64, COL ? ev : fev.w, COL ? fev.w : ev);
+                singular_warp<OP, HELM>(P.G64p, COL ? ev : fev.w, COL ? fev.w : ev);
             if (lane == src) val[u] = N::mk((T)sv.x, (T)sv.y);
             ++nsing;
           }

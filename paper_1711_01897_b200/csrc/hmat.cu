@@ -321,6 +321,7 @@ struct hbem_hmat {
   long long items_cap = 0;
   AcaDev S{};
   VPool vpool;  // ACA factor pool
+  Geo64 *g64p = nullptr;  // device copy of the context's float64 geometry view
   // pinned mailbox for the per-phase host reads
   struct Mail { Need tot; int n; int pad; } *mail = nullptr;
   // near-field leaves
@@ -492,6 +493,7 @@ template <typename T> Prob<T> make_prob(const hbem_hmat *H) {
   P.g = H->ctx->geo<T>();
   P.R = H->ctx->rule<T>();
   P.G64 = H->ctx->geo64();
+  P.G64p = H->g64p;
   P.elem = H->ctx->elem;
   P.rperm = H->rperm;
   P.cperm = H->cperm;
@@ -750,6 +752,11 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   tr.mark("near-field leaves");
   // ---- factor pool: virtual range of the free memory, mapped on demand
   size_t free_b = 0, total_b = 0;
+  {
+    Geo64 g = ctx->geo64();
+    HB_CHECK(dalloc(H, &H->g64p, 1));
+    HB_CUDA(cudaMemcpy(H->g64p, &g, sizeof(Geo64), cudaMemcpyHostToDevice));
+  }
   HB_CUDA(cudaFree(nullptr));
   HB_CUDA(cudaMemGetInfo(&free_b, &total_b));
   HB_CHECK(H->vpool.init(H->device, std::max<size_t>(free_b, (size_t)4 << 30)));

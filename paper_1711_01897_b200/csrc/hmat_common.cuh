@@ -138,6 +138,7 @@ template <typename T> struct Prob {
   const signed char *sloc;
   // P0: tree-ordered element records (test / trial tree; may alias)
   const T *trec, *srec;
+  const Geo64 *G64p;  // device copy of G64 (rarely used paths)
 };
 
 // block of one element pair (any adjacency), thread-level
@@ -301,7 +302,10 @@ __device__ __forceinline__ void p0_pairs_fx(const RuleTab<T> &R, const ElemRec<T
 // trial) in float64 (local_matrix, kernels.py:330-347), kept out of line so
 // its registers do not bound the occupancy of the regular path
 template <int OP, bool HELM>
-__device__ __noinline__ double2 singular_warp(const Geo64 G, int e, int f) {
+__device__ __noinline__ double2 singular_warp(const Geo64 *__restrict__ Gp, int e, int f) {
+  // the geometry view is read from global memory here, on the rare
+  // touching path, instead of being held in registers by every caller
+  const Geo64 G = *Gp;
   double re[1][1], im[1][1];
   singular_local<OP, HELM, 1, 1, 32>(G, e, f, re, im);
   return make_double2(re[0][0], im[0][0]);
