@@ -86,7 +86,9 @@ __global__ void k_need(AcaDev S, int na, int col) {
       head = key != (col ? S.rnode[bp] : S.cnode[bp]);
     }
     d.pool = (!col && S.pend[b] < 0) ? (long long)h + w + 1 : 0;
-    d.part = tiles * part_len(k, NC);
+    // statistics (4 per tile) + dots (k NC per tile), padded even so every
+    // job's records start 16-byte aligned
+    d.part = part_dots(tiles) + (((long long)tiles * k * NC + 1) & ~1ll);
     d.items = head ? tiles : 0;
   }
   S.need[p] = d;
@@ -268,11 +270,13 @@ __device__ __forceinline__ void aca_epi(const AcaDev &S, const JobS &J, const V_
 #if !(HB_EXPERIMENT & 1)
   warp_argmax_sum(best, bidx, ss);
 #endif
-  double *rec = S.part + J.part + (long long)t * part_len(k, NC);
+  const int nt = tiles_of(COL ? J.h : J.w);
+  double *stat = S.part + J.part + 4ll * t;
+  double *rec = S.part + J.part + part_dots(nt) + (long long)t * k * NC - 3;  // dots at rec[3 + l NC]
   if (lane == 0) {
-    rec[0] = best;
-    rec[1] = (double)bidx;
-    rec[2] = ss;
+    stat[0] = best;
+    stat[1] = (double)bidx;
+    stat[2] = ss;
   }
   // dots vdot(f_l, val) of the register batch: transposed reduction
   if (!(HB_EXPERIMENT & 2) && kk > 0) {
@@ -510,38 +514,26 @@ __global__ void __launch_bounds__(kThreads) k_aca_gen(Prob<T> P, AcaDev S, int n
 }
 
 // ---------------------------------------------------------------------------
-// finalize (thread per job; tiles combined in fixed tile order)
+// finalize, one warp per job: lanes over the job's tile records (statistics)
+// and over its terms (dots), both laid out contiguously per job, so every
+// load is coalesced; fixed-shape reductions keep the decisions deterministic.
 //
 // Term records are [u (h) | r (w) | p]: the residual row r is kept unscaled
 // and its pivot p stored behind it, v = r / p is applied where v is read
 // (residual coefficients, cross terms, payload packing).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void combine_tiles(const double *rec, int nt, long long RL,
-                                              double &best, int &bidx, double &ss) {
+__device__ __forceinline__ void combine_tiles_warp(const double *stats, int nt, int lane,
+                                                   double &best, int &bidx, double &ss) {
   best = -1.0;
   bidx = 0x7fffffff;
   ss = 0.0;
-#pragma unroll 4
-  for (int t = 0; t < nt; ++t) {
-    const double *r = rec + t * RL;
-    const double a = r[0];
-    const int ix = (int)r[1];
-    if (better(a, ix, best, bidx)) { best = a; bidx = ix; }
-    ss += r[2];
+  for (int t = lane; t < nt; t += 32) {
+    const double2 bi = *reinterpret_cast<const double2 *>(stats + 4ll * t);
+    const int ix = (int)bi.y;
+    if (better(bi.x, ix, best, bidx)) { best = bi.x; bidx = ix; }
+    ss += stats[4ll * t + 2];
   }
-}
-
-// sum of the dots of k terms over nt tile records (fixed tile order)
-template <int NC>
-__device__ __forceinline__ void sum_dots(const double *rec, int nt, long long RL, int l,
-                                         double &sr, double &si) {
-  sr = 0.0;
-  si = 0.0;
-#pragma unroll 4
-  for (int t = 0; t < nt; ++t) {
-    sr += rec[t * RL + 3 + (long long)l * NC];
-    if (NC == 2) si += rec[t * RL + 3 + (long long)l * NC + 1];
-  }
+  warp_argmax_sum(best, bidx, ss);
 }
 
 // row finalize: column pivot (hmatrix.py:329-332) or vanishing row (334-338)
@@ -549,17 +541,15 @@ template <typename T, bool C>
 __global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int n) {
   using N = Num<T, C>;
   using V = typename N::V;
-  constexpr int NC = N::NC;
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n) return;
   const Job J = S.jobs[p];
-  const int b = J.b, h = J.h, w = J.w, i = J.fix, k = J.k;
-  const int nt = tiles_of(w);
-  const long long RL = part_len(k, NC);
-  double *rec = S.part + J.part;
+  const int b = J.b, h = J.h, w = J.w, i = J.fix;
   double best, ss;
   int bidx;
-  combine_tiles(rec, nt, RL, best, bidx, ss);
+  combine_tiles_warp(S.part + J.part, tiles_of(w), lane, best, bidx, ss);
+  if (lane != 0) return;
   S.pend[b] = J.pe;
   if (best <= 0.0) {
     unsigned *rm = S.rmask + S.rmask_off[b];
@@ -591,16 +581,16 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
   using N = Num<T, C>;
   using V = typename N::V;
   constexpr int NC = N::NC;
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (p >= n) return;
   const Job J = S.jobs[p];
   const int b = J.b, h = J.h, w = J.w, j = J.fix, k = J.k, i = J.cur;
-  const int ntc = tiles_of(h);
-  const long long RL = part_len(k, NC);
+  const int ntc = tiles_of(h), ntr = tiles_of(w);
   const double *crec = S.part + J.part;
   double best, ss;
   int bidx;
-  combine_tiles(crec, ntc, RL, best, bidx, ss);
+  combine_tiles_warp(crec, ntc, lane, best, bidx, ss);
   const int next = best >= 0.0 ? bidx : -1;
   const double pr = S.piv[2 * b], pim = S.piv[2 * b + 1];
   const double nu = sqrt(ss);
@@ -610,34 +600,44 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
   const int kmax_b = min(S.kmax_cfg, min(h, w));
   unsigned *rm = S.rmask + S.rmask_off[b];
   if (n2 > 0.0 && upd <= S.eps * sqrt(n2)) {
-    S.resid[b] = upd / sqrt(n2);
-    const int sm = S.small[b] + 1;
-    S.small[b] = sm;
-    if (sm >= 2) {
-      S.status[b] = ST_CONVERGED;
-    } else {
-      set_bit(rm, i);
-      if (next < 0) {
+    if (lane == 0) {
+      S.resid[b] = upd / sqrt(n2);
+      const int sm = S.small[b] + 1;
+      S.small[b] = sm;
+      if (sm >= 2) {
         S.status[b] = ST_CONVERGED;
-        S.exhausted[b] = 1;
       } else {
-        S.cur[b] = next;
-        S.flagA[b] = 1;  // the pending record is reused
+        set_bit(rm, i);
+        if (next < 0) {
+          S.status[b] = ST_CONVERGED;
+          S.exhausted[b] = 1;
+        } else {
+          S.cur[b] = next;
+          S.flagA[b] = 1;  // the pending record is reused
+        }
       }
     }
     return;
   }
   // cross terms Re(vdot(u_l, u) vdot(v_l, v)) with v_l = r_l / p_l, v = r / p:
-  // vdot(v_l, v) = vdot(r_l, r) / (conj(p_l) p)
+  // vdot(v_l, v) = vdot(r_l, r) / (conj(p_l) p); lane l sums term l's dots
+  // over the column and row tiles in tile order
   const V *pool = static_cast<const V *>(S.pool);
-  const double *rrec = S.rpart + S.rowpart[b];
-  const int ntr = tiles_of(w);
+  const long long kn = (long long)k * NC;
+  const double *cd = crec + part_dots(ntc);
+  const double *rd = S.rpart + S.rowpart[b] + part_dots(ntr);
   const long long *tl = S.terms + (long long)b * S.tmax;
   double cross = 0.0;
-  for (int l = 0; l < k; ++l) {
-    double ur, ui, vr, vi;
-    sum_dots<NC>(crec, ntc, RL, l, ur, ui);
-    sum_dots<NC>(rrec, ntr, RL, l, vr, vi);
+  for (int l = lane; l < k; l += 32) {
+    double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
+    for (int t = 0; t < ntc; ++t) {
+      ur += cd[t * kn + (long long)l * NC];
+      if (C) ui += cd[t * kn + (long long)l * NC + 1];
+    }
+    for (int t = 0; t < ntr; ++t) {
+      vr += rd[t * kn + (long long)l * NC];
+      if (C) vi += rd[t * kn + (long long)l * NC + 1];
+    }
     const V pl = pool[tl[l] + h + w];
     const double plr = (double)N::re(pl), pli = (double)N::im(pl);
     const double dr = plr * pr + pli * pim, di = plr * pim - pli * pr;  // conj(p_l) p
@@ -652,6 +652,8 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
     }
     cross += ur * qr - ui * qi;
   }
+  cross = warp_sum_d(cross);
+  if (lane != 0) return;
   const double n2n = n2 + 2.0 * cross + upd * upd;
   S.norm2[b] = n2n;
   S.small[b] = 0;
@@ -756,7 +758,7 @@ int aca_phase(const Prob<T> &P, AcaDev &S, const PhaseArgs &A, int op, bool helm
     if (rc != HBEM_OK) return rc;
     if (A.int_end) HB_CUDA(cudaEventRecord(A.int_end, st));
   }
-  const unsigned fgrid = (unsigned)((n + kThreads - 1) / kThreads);
+  const unsigned fgrid = (unsigned)((n + kWarps - 1) / kWarps);
   if (col) k_fin_col<T, C><<<fgrid, kThreads, 0, st>>>(S, n);
   else k_fin_row<T, C><<<fgrid, kThreads, 0, st>>>(S, n);
   HB_CUDA(cudaGetLastError());

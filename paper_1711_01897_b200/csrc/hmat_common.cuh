@@ -373,7 +373,10 @@ struct Job {
 // partial record per (job, 32-wide tile): best |val| over unmasked entries,
 // its index, sum |val|^2, then k dots (re, im for complex) with the factor
 // the residual used: row phase vdot(v_l, row), column phase vdot(u_l, col).
-__host__ __device__ __forceinline__ long long part_len(int k, int nc) { return 3 + (long long)k * nc; }
+// per job: nt tile statistics records of 4 doubles (best |val| over unmasked,
+// its index, sum |val|^2, pad) followed by nt dot records of k*nc doubles
+__host__ __device__ __forceinline__ long long part_len(int k, int nc) { return 4 + (long long)k * nc; }
+__host__ __device__ __forceinline__ long long part_dots(int nt) { return 4ll * nt; }
 __host__ __device__ __forceinline__ int tiles_of(int n) { return (n + 31) >> 5; }
 
 struct Need {  // per-position allocation need (pool values, partial doubles, items)
