@@ -30,6 +30,9 @@
 namespace hb {
 
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef HB_JOB_GROUP
+#define HB_JOB_GROUP 2  // jobs whose quadratures run interleaved in k_aca_p0 (2 or 4)
+#endif
 #ifndef HB_EXPERIMENT
 #define HB_EXPERIMENT 0  // timing experiments only (bit 1: no tile argmax, 2: no dots, 4: no residual)
 #endif
@@ -349,12 +352,13 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
                                                         long long n_items) {
   using N = Num<T, C>;
   using V = typename N::V;
-  constexpr int kSeg = sizeof(V) > 8 ? 8 : 16;  // jobs staged per segment (48 KB static smem)
+  constexpr int kG = sizeof(V) > 8 ? 2 : HB_JOB_GROUP;  // jobs integrated together
+  constexpr int kSeg = (sizeof(V) > 8 || kG > 2) ? 8 : 16;  // jobs staged per segment (48 KB smem)
   __shared__ ElemRec<T> sr[kWarps][kSeg];
   __shared__ JobS sj[kWarps][kSeg];
   __shared__ long long sjt[kWarps][kSeg][kFinRegs];
   __shared__ V sjc[kWarps][kSeg][kFinRegs];
-  __shared__ V fbuf[kWarps][2][kFinRegs * 32];
+  __shared__ V fbuf[kWarps][kG][kFinRegs * 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long item = (long long)blockIdx.x * kWarps + wid;
   if (item >= n_items) return;
@@ -392,12 +396,14 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
     const unsigned okm = __ballot_sync(kFull, ok) | ~((1u << kSeg) - 1u);
     const int nseg = okm == kFull ? kSeg : __ffs(~okm) - 1;
     __syncwarp();
-    // jobs in pairs: two independent quadrature chains share the lane's points
-    for (int s = 0; s < nseg; s += 2) {
-      const int nj = s + 1 < nseg ? 2 : 1;
-      unsigned m[2];
+    // jobs in groups of kG (then 2, 1): independent quadrature chains that
+    // share the lane's points
+    for (int s = 0; s < nseg;) {
+      const int rem = nseg - s;
+      const int nj = rem >= kG ? kG : (rem >= 2 ? 2 : 1);
+      unsigned m[kG];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kG; ++u) {
         if (u < nj) {
           const JobS &J = sj[wid][s + u];
           const int kk = min(J.k, kFinRegs);
@@ -409,10 +415,18 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
           m[u] = masks[J.mofs + t];
         }
       }
-      V val[2];
-      if (nj == 2) {
+      V val[kG];
+      if (kG > 2 && nj == kG) {
+        const ElemRec<T> *FG[kG];
+#pragma unroll
+        for (int u = 0; u < kG; ++u) FG[u] = &sr[wid][s + u];
+        p0_pairs_fx<T, C, OP, HELM, !COL, kG>(P.R, FG, my.q, my.n, val);
+      } else if (nj == 2) {
         const ElemRec<T> *const F2[2] = {&sr[wid][s], &sr[wid][s + 1]};
-        p0_pairs_fx<T, C, OP, HELM, !COL, 2>(P.R, F2, my.q, my.n, val);
+        V v2[2];
+        p0_pairs_fx<T, C, OP, HELM, !COL, 2>(P.R, F2, my.q, my.n, v2);
+        val[0] = v2[0];
+        val[1] = v2[1];
       } else {
         const ElemRec<T> *const F1[1] = {&sr[wid][s]};
         V v1[1];
@@ -420,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
         val[0] = v1[0];
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kG; ++u) {
         if (u < nj) {
           const int4 fev = sr[wid][s + u].ev;
           unsigned tm = __ballot_sync(kFull, valid && touching4(my.ev, fev));
@@ -437,10 +451,11 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
       }
       cp_async_wait_all();
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int u = 0; u < kG; ++u)
         if (u < nj)
           aca_epi<T, C, COL>(S, sj[wid][s + u], sjc[wid][s + u], t, lane, valid, val[u],
                              fbuf[wid][u], m[u]);
+      s += nj;
     }
     nent += valid ? nseg : 0;
     __syncwarp();
@@ -629,16 +644,18 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
   const long long *tl = S.terms + (long long)b * S.tmax;
   double cross = 0.0;
   for (int l = lane; l < k; l += 32) {
+    const V pl = pool[tl[l] + h + w];  // issued first: two dependent loads
     double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
+#pragma unroll 8
     for (int t = 0; t < ntc; ++t) {
       ur += cd[t * kn + (long long)l * NC];
       if (C) ui += cd[t * kn + (long long)l * NC + 1];
     }
+#pragma unroll 8
     for (int t = 0; t < ntr; ++t) {
       vr += rd[t * kn + (long long)l * NC];
       if (C) vi += rd[t * kn + (long long)l * NC + 1];
     }
-    const V pl = pool[tl[l] + h + w];
     const double plr = (double)N::re(pl), pli = (double)N::im(pl);
     const double dr = plr * pr + pli * pim, di = plr * pim - pli * pr;  // conj(p_l) p
     double qr, qi;
