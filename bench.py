@@ -348,6 +348,11 @@ def run_ours(args):
                "sample": f"{nl} C5 leaves drawn cost-weighted ({reg} regular + {sg} singular "
                          f"pairs in {wall:.1f} s), oracle on 1 core",
                "extrapolated_assembly_s": (stats["regular_pairs"] + stats["singular_pairs"]) / rate}
+        # release the oracle's millions of Python objects before the e2e
+        # timing (the cyclic GC would otherwise scan them mid-measurement)
+        import gc
+        _G.clear()
+        gc.collect()
 
     e2e = None
     if not args.no_e2e:
