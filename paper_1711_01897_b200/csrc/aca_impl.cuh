@@ -91,7 +91,7 @@ __global__ void k_need(AcaDev S, int na, int col) {
     d.pool = (!col && S.pend[b] < 0) ? (long long)h + w + 1 : 0;
     // statistics (4 per tile) + dots (k NC per tile), padded even so every
     // job's records start 16-byte aligned
-    d.part = part_dots(tiles) + (((long long)tiles * k * NC + 1) & ~1ll);
+    d.part = ((long long)tiles * k * NC + 1) & ~1ll;
     d.items = head ? tiles : 0;
   }
   S.need[p] = d;
@@ -244,7 +244,7 @@ struct JobS {
 template <typename T, bool C, bool COL>
 __device__ __forceinline__ void aca_epi(const AcaDev &S, const JobS &J, const V_t<T, C> *cs,
                                         int t, int lane, bool valid, V_t<T, C> val,
-                                        const V_t<T, C> *fb, unsigned m) {
+                                        const V_t<T, C> *fb) {
   using N = Num<T, C>;
   using V = typename N::V;
   constexpr int NC = N::NC;
@@ -265,22 +265,10 @@ __device__ __forceinline__ void aca_epi(const AcaDev &S, const JobS &J, const V_
     if (valid) val = N::fms(val, c, pool[tb + ro + idx]);
   }
   if (valid) pool[J.pe + (COL ? 0 : J.h) + idx] = val;
-  // tile statistics
-  const bool masked = ((m >> lane) & 1u) || (COL && idx == J.cur);
-  double best = (valid && !masked) ? N::abs(val) : -1.0;
-  int bidx = (valid && !masked) ? idx : 0x7fffffff;
-  double ss = valid ? N::nrm(val) : 0.0;
-#if !(HB_EXPERIMENT & 1)
-  warp_argmax_sum(best, bidx, ss);
-#endif
+  // dot records of this tile: k (x2 complex) values at rec[3 + l NC]
   const int nt = tiles_of(COL ? J.h : J.w);
-  double *stat = S.part + J.part + 4ll * t;
-  double *rec = S.part + J.part + part_dots(nt) + (long long)t * k * NC - 3;  // dots at rec[3 + l NC]
-  if (lane == 0) {
-    stat[0] = best;
-    stat[1] = (double)bidx;
-    stat[2] = ss;
-  }
+  (void)nt;
+  double *rec = S.part + J.part + (long long)t * k * NC - 3;
   // dots vdot(f_l, val) of the register batch: transposed reduction
   if (!(HB_EXPERIMENT & 2) && kk > 0) {
     double dr[8], di[8];
@@ -371,7 +359,6 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
   ElemRec<T> my;
   load_rec<T>(COL ? P.trec : P.srec, vstart + (valid ? idx : nvar - 1), my);
   const V *pool = static_cast<const V *>(S.pool);
-  const unsigned *masks = COL ? S.rmask : S.cmask;
   unsigned long long nent = 0, nsing = 0;
   for (int seg = p0;; seg += kSeg) {
     bool ok = false;
@@ -401,7 +388,6 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
     for (int s = 0; s < nseg;) {
       const int rem = nseg - s;
       const int nj = rem >= kG ? kG : (rem >= 2 ? 2 : 1);
-      unsigned m[kG];
 #pragma unroll
       for (int u = 0; u < kG; ++u) {
         if (u < nj) {
@@ -412,7 +398,6 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
           for (int l = 0; l < kFinRegs; ++l)
             if (l < kk && valid)
               cp_async<sizeof(V)>(&fbuf[wid][u][l * 32 + lane], pool + sjt[wid][s + u][l] + ro + idx);
-          m[u] = masks[J.mofs + t];
         }
       }
       V val[kG];
@@ -454,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
       for (int u = 0; u < kG; ++u)
         if (u < nj)
           aca_epi<T, C, COL>(S, sj[wid][s + u], sjc[wid][s + u], t, lane, valid, val[u],
-                             fbuf[wid][u], m[u]);
+                             fbuf[wid][u]);
       s += nj;
     }
     nent += valid ? nseg : 0;
@@ -488,7 +473,6 @@ __global__ void __launch_bounds__(kThreads) k_aca_gen(Prob<T> P, AcaDev S, int n
   const bool valid = idx < J0.nvar;
   const int vdof = valid ? (COL ? P.rperm : P.cperm)[J0.vstart + idx] : 0;
   const V *pool = static_cast<const V *>(S.pool);
-  const unsigned *masks = COL ? S.rmask : S.cmask;
   unsigned long long nent = 0;
   for (int p = p0;; ++p) {
     bool ok = false;
@@ -513,14 +497,13 @@ __global__ void __launch_bounds__(kThreads) k_aca_gen(Prob<T> P, AcaDev S, int n
 #pragma unroll
     for (int l = 0; l < kFinRegs; ++l)
       if (l < kk && valid) cp_async<sizeof(V)>(&fbuf[wid][l * 32 + lane], pool + gjt[l] + ro + idx);
-    const unsigned m = masks[J.mofs + t];
     const int fdof = COL ? P.cperm[S.c0[J.b] + J.fix] : P.rperm[S.r0[J.b] + J.fix];
     V val = N::zero();
     if (valid)
       val = COL ? entry<T, C, OP, HELM, NT, NS>(P, vdof, fdof, S.stat + 1)
                 : entry<T, C, OP, HELM, NT, NS>(P, fdof, vdof, S.stat + 1);
     cp_async_wait_all();
-    aca_epi<T, C, COL>(S, J, sjc[wid], t, lane, valid, val, fbuf[wid], m);
+    aca_epi<T, C, COL>(S, J, sjc[wid], t, lane, valid, val, fbuf[wid]);
     nent += valid ? 1 : 0;
     __syncwarp();
   }
@@ -537,16 +520,37 @@ __global__ void __launch_bounds__(kThreads) k_aca_gen(Prob<T> P, AcaDev S, int n
 // and its pivot p stored behind it, v = r / p is applied where v is read
 // (residual coefficients, cross terms, payload packing).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void combine_tiles_warp(const double *stats, int nt, int lane,
-                                                   double &best, int &bidx, double &ss) {
+// pivot statistics of a residual row / column, lanes over its entries in
+// order: argmax |val| over unmasked entries (first index on ties) and
+// sum |val|^2 over all entries (hmatrix.py:329-332 / 301-314, 343-362)
+template <typename T, bool C>
+__device__ __forceinline__ void residual_stats(const typename Num<T, C>::V *vals, int n,
+                                               const unsigned *mask, int skip, int lane,
+                                               double &best, int &bidx, double &ss) {
+  using N = Num<T, C>;
   best = -1.0;
   bidx = 0x7fffffff;
   ss = 0.0;
-  for (int t = lane; t < nt; t += 32) {
-    const double2 bi = *reinterpret_cast<const double2 *>(stats + 4ll * t);
-    const int ix = (int)bi.y;
-    if (better(bi.x, ix, best, bidx)) { best = bi.x; bidx = ix; }
-    ss += stats[4ll * t + 2];
+  // four chunks of 32 per step: their loads are issued together
+  for (int i0 = 0; i0 < n; i0 += 128) {
+    typename N::V v[4];
+    unsigned mw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + 32 * u + lane;
+      v[u] = i < n ? vals[i] : N::zero();
+      mw[u] = i0 + 32 * u < n ? mask[(i0 >> 5) + u] : ~0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + 32 * u + lane;
+      if (i < n) {
+        const double a = N::abs(v[u]);
+        ss += N::nrm(v[u]);
+        const bool masked = ((mw[u] >> lane) & 1u) || i == skip;
+        if (!masked && a > best) { best = a; bidx = i; }
+      }
+    }
   }
   warp_argmax_sum(best, bidx, ss);
 }
@@ -563,7 +567,8 @@ __global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int n) {
   const int b = J.b, h = J.h, w = J.w, i = J.fix;
   double best, ss;
   int bidx;
-  combine_tiles_warp(S.part + J.part, tiles_of(w), lane, best, bidx, ss);
+  const V *pool = static_cast<const V *>(S.pool);
+  residual_stats<T, C>(pool + J.pe + h, w, S.cmask + S.cmask_off[b], -1, lane, best, bidx, ss);
   if (lane != 0) return;
   S.pend[b] = J.pe;
   if (best <= 0.0) {
@@ -579,9 +584,9 @@ __global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int n) {
     }
     return;
   }
-  V *pool = static_cast<V *>(S.pool);
-  const V pv = pool[J.pe + h + bidx];
-  pool[J.pe + h + w] = pv;
+  V *wpool = static_cast<V *>(S.pool);
+  const V pv = wpool[J.pe + h + bidx];
+  wpool[J.pe + h + w] = pv;
   S.pcol[b] = bidx;
   S.piv[2 * b] = (double)N::re(pv);
   S.piv[2 * b + 1] = (double)N::im(pv);
@@ -603,9 +608,10 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
   const int b = J.b, h = J.h, w = J.w, j = J.fix, k = J.k, i = J.cur;
   const int ntc = tiles_of(h), ntr = tiles_of(w);
   const double *crec = S.part + J.part;
+  const V *pool = static_cast<const V *>(S.pool);
   double best, ss;
   int bidx;
-  combine_tiles_warp(crec, ntc, lane, best, bidx, ss);
+  residual_stats<T, C>(pool + J.pe, h, S.rmask + S.rmask_off[b], i, lane, best, bidx, ss);
   const int next = best >= 0.0 ? bidx : -1;
   const double pr = S.piv[2 * b], pim = S.piv[2 * b + 1];
   const double nu = sqrt(ss);
@@ -637,25 +643,13 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
   // cross terms Re(vdot(u_l, u) vdot(v_l, v)) with v_l = r_l / p_l, v = r / p:
   // vdot(v_l, v) = vdot(r_l, r) / (conj(p_l) p); lane l sums term l's dots
   // over the column and row tiles in tile order
-  const V *pool = static_cast<const V *>(S.pool);
   const long long kn = (long long)k * NC;
-  const double *cd = crec + part_dots(ntc);
-  const double *rd = S.rpart + S.rowpart[b] + part_dots(ntr);
+  const double *cd = crec;
+  const double *rd = S.rpart + S.rowpart[b];
   const long long *tl = S.terms + (long long)b * S.tmax;
   double cross = 0.0;
-  for (int l = lane; l < k; l += 32) {
-    const V pl = pool[tl[l] + h + w];  // issued first: two dependent loads
-    double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
-#pragma unroll 8
-    for (int t = 0; t < ntc; ++t) {
-      ur += cd[t * kn + (long long)l * NC];
-      if (C) ui += cd[t * kn + (long long)l * NC + 1];
-    }
-#pragma unroll 8
-    for (int t = 0; t < ntr; ++t) {
-      vr += rd[t * kn + (long long)l * NC];
-      if (C) vi += rd[t * kn + (long long)l * NC + 1];
-    }
+  auto cross_term = [&](int l, double ur, double ui, double vr, double vi) {
+    const V pl = pool[tl[l] + h + w];
     const double plr = (double)N::re(pl), pli = (double)N::im(pl);
     const double dr = plr * pr + pli * pim, di = plr * pim - pli * pr;  // conj(p_l) p
     double qr, qi;
@@ -667,7 +661,47 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
       qr = vr / dr;
       qi = 0.0;
     }
-    cross += ur * qr - ui * qi;
+    return ur * qr - ui * qi;
+  };
+  if (k <= 8) {
+    // lanes over tiles, 8 term accumulators per lane, one transposed
+    // reduction per plane (tile order within a lane, fixed tree across lanes)
+    double ur[8], ui[8], vr[8], vi[8];
+#pragma unroll
+    for (int l = 0; l < 8; ++l) { ur[l] = 0.0; ui[l] = 0.0; vr[l] = 0.0; vi[l] = 0.0; }
+    for (int t = lane; t < ntc; t += 32)
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        if (l < k) {
+          ur[l] += cd[t * kn + (long long)l * NC];
+          if (C) ui[l] += cd[t * kn + (long long)l * NC + 1];
+        }
+    for (int t = lane; t < ntr; t += 32)
+#pragma unroll
+      for (int l = 0; l < 8; ++l)
+        if (l < k) {
+          vr[l] += rd[t * kn + (long long)l * NC];
+          if (C) vi[l] += rd[t * kn + (long long)l * NC + 1];
+        }
+    const double tur = tr_reduce8(ur, lane), tvr = tr_reduce8(vr, lane);
+    const double tui = C ? tr_reduce8(ui, lane) : 0.0, tvi = C ? tr_reduce8(vi, lane) : 0.0;
+    const int l = lane >> 2;
+    if ((lane & 3) == 0 && l < k) cross = cross_term(l, tur, tui, tvr, tvi);
+  } else {
+    for (int l = lane; l < k; l += 32) {
+      double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
+#pragma unroll 8
+      for (int t = 0; t < ntc; ++t) {
+        ur += cd[t * kn + (long long)l * NC];
+        if (C) ui += cd[t * kn + (long long)l * NC + 1];
+      }
+#pragma unroll 8
+      for (int t = 0; t < ntr; ++t) {
+        vr += rd[t * kn + (long long)l * NC];
+        if (C) vi += rd[t * kn + (long long)l * NC + 1];
+      }
+      cross += cross_term(l, ur, ui, vr, vi);
+    }
   }
   cross = warp_sum_d(cross);
   if (lane != 0) return;
