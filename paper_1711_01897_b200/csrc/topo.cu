@@ -14,7 +14,7 @@
 namespace hb {
 namespace {
 
-constexpr int kMaxNb = 64;  // touching elements per element (valence bound)
+constexpr int kMaxNb = 1024;  // touching elements per element (setup scratch bound)
 
 __global__ void k_corner_keys(const int4 *elem, int m, unsigned long long *keys) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;

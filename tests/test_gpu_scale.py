@@ -127,3 +127,20 @@ def test_hull_mesh_assembly_vs_exact_rows():
     rows = rng.choice(sp.n_dofs, size=6, replace=False)
     z = exact_rows(spec, sp, rows, x)
     assert np.abs(y[rows] - z).max() <= 10 * eps * np.sqrt(np.mean(np.abs(y) ** 2))
+
+
+def test_hull_hmatrix_matches_reference():
+    """Golden from the real reference (tests/golden/make_hull_golden.py):
+    elongated hull, Helmholtz SLP P0, 8 elements per wavelength, eps 1e-3.
+    Same ACA pivots => the device H-matrix matvec equals the reference's
+    H-matrix matvec to rounding (the ACA error itself is ~6e-3 here)."""
+    from conftest import golden
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix
+    from paper_1711_01897_b200.meshes import elongated_hull
+    g = golden("hull")
+    v, e = elongated_hull(int(g["n_around"]), int(g["n_along"]))
+    _, _, spec, sp, bt = problem((v, e), "p0", "helmholtz", "slp", float(g["k"]))
+    h = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=float(g["eps"])))
+    for x, yr in zip(g["x"], g["y"]):
+        y = h.matvec(x)
+        assert np.abs(y - yr).max() <= 1e-10 * np.abs(yr).max()
