@@ -15,7 +15,7 @@
 #include "hbem_internal.h"
 
 #ifndef HB_INNER_UNROLL2
-#define HB_INNER_UNROLL2 2  // fixed-point loop unroll of the two-job quadrature
+#define HB_INNER_UNROLL2 6  // fixed-point loop unroll of the two-job quadrature
 #endif
 #ifndef HB_ACA_MINB
 #define HB_ACA_MINB 3  // k_aca_p0 / k_near_p0 resident CTAs per SM (register cap)
