@@ -364,6 +364,7 @@ struct hbem_hmat {
   cudaStream_t cp = nullptr;    // factor packing + D2H, middle priority
   cudaStream_t cpd = nullptr;   // dense-arena D2H (waits for the near field)
   cudaEvent_t emit_ev = nullptr;
+  cudaEvent_t tab_done = nullptr;  // singular table complete (side stream)
   cudaStream_t side = nullptr;  // near-field leaves, lowest priority
   cudaStream_t hi = nullptr;    // ACA waves, highest priority
   cudaEvent_t side_done = nullptr;
@@ -392,6 +393,7 @@ struct hbem_hmat {
     if (cp) cudaStreamDestroy(cp);
     if (cpd) cudaStreamDestroy(cpd);
     if (emit_ev) cudaEventDestroy(emit_ev);
+    if (tab_done) cudaEventDestroy(tab_done);
     if (side_done) cudaEventDestroy(side_done);
     for (auto e : ev)
       if (e) cudaEventDestroy(e);
@@ -494,6 +496,9 @@ template <typename T> Prob<T> make_prob(const hbem_hmat *H) {
   P.R = H->ctx->rule<T>();
   P.G64 = H->ctx->geo64();
   P.G64p = H->g64p;
+  P.nb_ptr = H->D.nb_ptr;
+  P.nb_idx = H->D.nb_idx;
+  P.stab = H->D.stab;
   P.elem = H->ctx->elem;
   P.rperm = H->rperm;
   P.cperm = H->cperm;
@@ -705,19 +710,22 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
     HB_CHECK(upload(H, &pl, doff)); D.off = pl;
     HB_CHECK(dalloc(H, &D.sing_count, 1));
     HB_CHECK(dalloc(H, &D.stat, 2));
-    if (H->p0 && nd > 0) {
+    if ((H->p0 && nd > 0) || !H->p0) {
       // touching element pairs integrated once per execute into a table the
       // near-field kernel reads (single layer: each unordered pair once)
       SingTable tab;
       tr.mark("near-field arrays");
-      HB_CHECK(build_sing_table(ctx->elem, (int)m, (int)ctx->nv, ctx->op == HBEM_SLP, tab,
-                                H->dev_allocs, 0));
+      // symmetric operators on equal spaces: S(f, e) = S(e, f)^T bit for bit
+      // (canonical orientation, kernels.py:340-344), one integration per pair
+      const bool sym = (ctx->op == HBEM_SLP || ctx->op == HBEM_HYPS) && nt == ns &&
+                       ctx->test_family == ctx->trial_family;
+      HB_CHECK(build_sing_table(ctx->elem, (int)m, (int)ctx->nv, sym, tab, H->dev_allocs, 0));
       D.nb_ptr = tab.nb_ptr;
       D.nb_idx = tab.nb_idx;
       D.spairs = tab.pairs;
       D.n_spairs = tab.n_pairs;
       char *st_vals = nullptr;
-      HB_CHECK(dalloc(H, &st_vals, (size_t)tab.nnz * H->vbytes));
+      HB_CHECK(dalloc(H, &st_vals, (size_t)tab.nnz * nt * ns * H->vbytes));
       D.stab = st_vals;
       tr.mark("singular table topology");
     }
@@ -778,6 +786,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
                                          greatest < least ? greatest + 1 : least));
     HB_CUDA(cudaStreamCreateWithPriority(&H->cpd, cudaStreamNonBlocking, least));
     HB_CUDA(cudaEventCreateWithFlags(&H->emit_ev, cudaEventDisableTiming));
+    HB_CUDA(cudaEventCreateWithFlags(&H->tab_done, cudaEventDisableTiming));
   }
   // streamed payload arenas (virtual ranges, mapped as blocks converge)
   HB_CHECK(H->uarena.init(H->device, std::max<size_t>(free_b / 2, (size_t)4 << 30)));
@@ -968,13 +977,18 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   HB_CUDA(cudaStreamWaitEvent(H->side, start_ev, 0));
   cudaEventDestroy(start_ev);
   HB_CUDA(cudaEventRecord(H->ev[2], H->side));
+  if (H->D.n_spairs > 0) {
+    HB_CHECK((sing_table_launch<T, C>(P, H->D, ctx->op, ctx->helm, nt, ns, H->side)));
+    ++launches;
+  }
+  HB_CUDA(cudaEventRecord(H->tab_done, H->side));
+  if (!H->p0) HB_CUDA(cudaStreamWaitEvent(st, H->tab_done, 0));  // k_aca_gen reads the table
   if (H->nd > 0) {
     HB_CUDA(cudaMemsetAsync(H->D.sing_count, 0, 8, H->side));
     HB_CUDA(cudaMemsetAsync(H->D.stat, 0, 16, H->side));
     if (H->p0) {
-      HB_CHECK((sing_table_launch<T, C>(P, H->D, ctx->op, ctx->helm, H->side)));
       HB_CHECK((near_p0_launch<T, C>(P, H->D, ctx->op, ctx->helm, H->side)));
-      launches += 2;
+      launches += 1;
     } else {
       int rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc,
                                                            auto NSc) -> int {
@@ -1042,6 +1056,7 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
     HB_CHECK((emit_converged<T, C>(H, st, /*pack=*/false)));
   }
   H->packed = H->streaming();
+  HB_CUDA(cudaStreamWaitEvent(st, H->tab_done, 0));  // fallback rows may read the table
   const auto t_aca = clk::now();
   // ---- classify admissible blocks (lowrank_leaf, hmatrix.py:721-735) -------------
   std::vector<int> st_h(na), rk_h(na), ex_h(na);

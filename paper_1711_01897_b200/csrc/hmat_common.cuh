@@ -139,6 +139,9 @@ template <typename T> struct Prob {
   // P0: tree-ordered element records (test / trial tree; may alias)
   const T *trec, *srec;
   const Geo64 *G64p;  // device copy of G64 (rarely used paths)
+  // singular table (k_sing_table): touching element pairs -> NT x NS block
+  const int *nb_ptr, *nb_idx;
+  const void *stab;
 };
 
 // block of one element pair (any adjacency), thread-level
@@ -146,6 +149,23 @@ template <typename T, int OP, bool HELM, int NT, int NS>
 __device__ __forceinline__ void pair_block(const Prob<T> &P, int e, int f, T (&re)[NT][NS],
                                            T (&im)[NT][NS], unsigned long long *nsing) {
   if (touching(P.elem[e], P.elem[f])) {
+    if (P.stab) {
+      // Sauter-Schwab block from the singular table (one integration per
+      // touching element pair and execute, warp-cooperative)
+      int j = P.nb_ptr[e];
+      while (P.nb_idx[j] != f) ++j;
+      const T *blk = static_cast<const T *>(P.stab) + (long long)j * NT * NS * (HELM ? 2 : 1);
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int jj = 0; jj < NS; ++jj) {
+          const int o = i * NS + jj;
+          re[i][jj] = HELM ? blk[2 * o] : blk[o];
+          im[i][jj] = HELM ? blk[2 * o + 1] : T(0);
+        }
+      if (nsing) atomicAdd(nsing, 1ull);
+      return;
+    }
     double dr[NT][NS], di[NT][NS];
     singular_local<OP, HELM, NT, NS, 1>(P.G64, e, f, dr, di);
 #pragma unroll
@@ -495,7 +515,8 @@ struct MatvecArgs {
 template <typename T, bool C>
 int matvec_launch(const MatvecArgs &M, const AcaDev &S, cudaStream_t st);
 template <typename T, bool C>
-int sing_table_launch(const Prob<T> &P, const DenseDev &D, int op, bool helm, cudaStream_t st);
+int sing_table_launch(const Prob<T> &P, const DenseDev &D, int op, bool helm, int nt, int ns,
+                      cudaStream_t st);
 template <typename T, bool C>
 int near_p0_launch(const Prob<T> &P, const DenseDev &D, int op, bool helm, cudaStream_t st);
 

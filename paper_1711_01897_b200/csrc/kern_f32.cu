@@ -21,9 +21,9 @@ template int near_p0_launch<float, true>(const Prob<float> &, const DenseDev &, 
                                           cudaStream_t);
 template int build_recs<float>(const Geo<float> &, const int4 *, const int *, int, float *,
                                 cudaStream_t);
-template int sing_table_launch<float, false>(const Prob<float> &, const DenseDev &, int, bool,
+template int sing_table_launch<float, false>(const Prob<float> &, const DenseDev &, int, bool, int, int,
                                              cudaStream_t);
-template int sing_table_launch<float, true>(const Prob<float> &, const DenseDev &, int, bool,
+template int sing_table_launch<float, true>(const Prob<float> &, const DenseDev &, int, bool, int, int,
                                             cudaStream_t);
 template int matvec_launch<float, false>(const MatvecArgs &, const AcaDev &, cudaStream_t);
 template int matvec_launch<float, true>(const MatvecArgs &, const AcaDev &, cudaStream_t);

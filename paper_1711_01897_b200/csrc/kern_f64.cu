@@ -22,9 +22,9 @@ template int near_p0_launch<double, true>(const Prob<double> &, const DenseDev &
                                           cudaStream_t);
 template int build_recs<double>(const Geo<double> &, const int4 *, const int *, int, double *,
                                 cudaStream_t);
-template int sing_table_launch<double, false>(const Prob<double> &, const DenseDev &, int, bool,
+template int sing_table_launch<double, false>(const Prob<double> &, const DenseDev &, int, bool, int, int,
                                              cudaStream_t);
-template int sing_table_launch<double, true>(const Prob<double> &, const DenseDev &, int, bool,
+template int sing_table_launch<double, true>(const Prob<double> &, const DenseDev &, int, bool, int, int,
                                             cudaStream_t);
 template int matvec_launch<double, false>(const MatvecArgs &, const AcaDev &, cudaStream_t);
 template int matvec_launch<double, true>(const MatvecArgs &, const AcaDev &, cudaStream_t);

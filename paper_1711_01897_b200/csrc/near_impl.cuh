@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_near_p0(Prob<T> P, De
 // (S = S^T, kernels.py:340-344), so it is also stored at (f, e) and each
 // unordered pair is integrated once.
 // ---------------------------------------------------------------------------
-template <typename T, bool C, int OP, bool HELM>
+template <typename T, bool C, int OP, bool HELM, int NT, int NS>
 __global__ void __launch_bounds__(kThreads) k_sing_table(Prob<T> P, DenseDev D) {
   using N = Num<T, C>;
   using V = typename N::V;
@@ -114,32 +114,41 @@ __global__ void __launch_bounds__(kThreads) k_sing_table(Prob<T> P, DenseDev D) 
   V *tab = static_cast<V *>(D.stab);
   for (long long q = warp; q < D.n_spairs; q += nw) {
     const int4 pr = D.spairs[q];
-    double re[1][1], im[1][1];
-    singular_local<OP, HELM, 1, 1, 32>(P.G64, pr.x, pr.y, re, im);
-    if (lane == 0) {
-      const V v = N::mk((T)re[0][0], (T)im[0][0]);
-      tab[pr.z] = v;
-      if (pr.w >= 0) tab[pr.w] = v;
-    }
+    double re[NT][NS], im[NT][NS];
+    singular_local<OP, HELM, NT, NS, 32>(P.G64, pr.x, pr.y, re, im);
+    // lane o < NT NS stores entry o of the block (and of its transpose at
+    // the back slot: the symmetric operators give S(f,e) = S(e,f)^T)
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+        if (lane == i * NS + j) {
+          const V v = N::mk((T)re[i][j], (T)im[i][j]);
+          tab[(long long)pr.z * NT * NS + i * NS + j] = v;
+          if (pr.w >= 0) tab[(long long)pr.w * NT * NS + j * NT + i] = v;
+        }
+      }
   }
 }
 
 template <typename T, bool C>
-int sing_table_launch(const Prob<T> &P, const DenseDev &D, int op, bool helm, cudaStream_t st) {
+int sing_table_launch(const Prob<T> &P, const DenseDev &D, int op, bool helm, int nt, int ns,
+                      cudaStream_t st) {
   if (D.n_spairs <= 0) return HBEM_OK;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const unsigned grid =
       (unsigned)std::min<long long>((D.n_spairs + kWarps - 1) / kWarps, (long long)sms * 16);
-  return dispatch_op(op, helm, 1, 1, [&](auto OPc, auto Hc, auto, auto) -> int {
+  return dispatch_op(op, helm, nt, ns, [&](auto OPc, auto Hc, auto NTc, auto NSc) -> int {
     constexpr int OP = decltype(OPc)::value;
     constexpr bool HH = decltype(Hc)::value != 0;
-    if constexpr (HH == C && OP != HBEM_HYPS) {
-      k_sing_table<T, C, OP, HH><<<grid, kThreads, 0, st>>>(P, D);
+    constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
+    if constexpr (HH == C) {
+      k_sing_table<T, C, OP, HH, NT, NS><<<grid, kThreads, 0, st>>>(P, D);
       HB_CUDA(cudaGetLastError());
       return HBEM_OK;
     } else {
-      return set_error(HBEM_ERR_KERNEL, "unsupported P0 singular-table operator");
+      return set_error(HBEM_ERR_KERNEL, "value type does not match the equation");
     }
   });
 }
