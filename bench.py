@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="bounded CPU sample per baseline measurement")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-reps", type=int, default=3, help="end-to-end repetitions (median)")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
@@ -365,32 +366,42 @@ def run_ours(args):
         part.close()
         del part
         dev.close()
-        barrier()
-        t0 = time.perf_counter()
-        dev2 = init_gpu_device(ictx, local)
-        t1 = time.perf_counter()
-        # payloads streamed wave by wave into the page-locked host arenas
-        part2 = _assemble_part(dev2, bt, ids, sp, sp, cfg, acfg, stream=sptr, out=pinned)
-        t2 = time.perf_counter()
-        s2 = part2.stats
-        got = part2.arenas()
-        assert all(len(g) == n for g, n in zip(got, (s2["u_entries"], s2["v_entries"],
-                                                      s2["dense_entries"])))
-        torch.cuda.synchronize()
-        t3 = time.perf_counter()
-        t_e2e = t3 - t0
-        split = {"context_s": t1 - t0, "setup_s": float(s2["seconds_setup"]),
-                 "assemble_s": float(s2["seconds"]),
-                 "plan_assemble_and_streamed_d2h_s": t2 - t1, "tail_s": t3 - t2}
-        if dist is not None:
-            tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t_e2e = float(tt.item())
-        e2e = {"value": pairs / args.steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "seconds": t_e2e, "split": split,
+        samples, splits = [], []
+        part2 = None
+        for rep in range(max(args.e2e_reps, 1)):
+            if part2 is not None:
+                part2.close()
+                dev2.close()
+            barrier()
+            t0 = time.perf_counter()
+            dev2 = init_gpu_device(ictx, local)
+            t1 = time.perf_counter()
+            # payloads streamed wave by wave into the page-locked host arenas
+            part2 = _assemble_part(dev2, bt, ids, sp, sp, cfg, acfg, stream=sptr, out=pinned)
+            t2 = time.perf_counter()
+            s2 = part2.stats
+            got = part2.arenas()
+            assert all(len(g) == n for g, n in zip(got, (s2["u_entries"], s2["v_entries"],
+                                                          s2["dense_entries"])))
+            torch.cuda.synchronize()
+            t3 = time.perf_counter()
+            t_e2e = t3 - t0
+            if dist is not None:
+                tt = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t_e2e = float(tt.item())
+            samples.append(t_e2e)
+            splits.append({"context_s": t1 - t0, "setup_s": float(s2["seconds_setup"]),
+                           "assemble_s": float(s2["seconds"]),
+                           "plan_assemble_and_streamed_d2h_s": t2 - t1, "tail_s": t3 - t2})
+        med = float(np.median(samples))
+        e2e = {"value": pairs / args.steps / med, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "seconds": med, "samples_s": samples,
+               "split": splits[int(np.argsort(samples)[len(samples) // 2])],
                "path": "GpuDeviceContext + assemble (hbem_ctx_create, hbem_hmat_assemble "
                        "with page-locked host output arenas: factors streamed per ACA wave, "
-                       "dense leaves when the near field completes)"}
+                       "dense leaves when the near field completes); median of "
+                       f"{len(samples)} repetitions"}
         part = part2
 
     if rank == 0:
