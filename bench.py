@@ -52,6 +52,18 @@ FLOP_PER_PAIR_LAP_SLP_P0 = 360
 DP_INSTR_PER_PAIR = 12 * 36 + 2
 
 
+def _ncu_traffic():
+    """DRAM bytes per k_aca_p0 launch (dram__bytes_read.sum + dram__bytes_write.sum,
+    averaged over the 30 launches of one C5 FP64 assembly) from the committed ncu
+    capture profiles/r01_traffic_k_aca_p0.json; None when absent."""
+    p = os.path.join(ROOT, "profiles", "r01_traffic_k_aca_p0.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["dram_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -327,7 +339,7 @@ def run_ours(args):
                 "kernel": "k_aca_p0 (ACA row/column integration, fused residual + tile statistics)",
                 "achieved": flop_rate / 1e12, "peak": peak.value / 1e12, "unit": "TFLOP/s",
                 "frac": flop_rate / peak.value if peak.value else None,
-                "traffic": None,
+                "traffic": _ncu_traffic(),
                 "peak_source": "measured live on this GPU: hbem_probe_fma (independent DFMA "
                                "chains, 2 FLOP per FMA); MEASURED_PEAKS.json has no FP64 figure",
                 "algorithmic": f"{FLOP_PER_PAIR_LAP_SLP_P0} FLOP per regular pair (SURVEY 8d) x "
