@@ -977,13 +977,14 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   HB_CUDA(cudaStreamWaitEvent(H->side, start_ev, 0));
   cudaEventDestroy(start_ev);
   HB_CUDA(cudaEventRecord(H->ev[2], H->side));
-  if (H->D.n_spairs > 0) {
+  const bool skip_nf = std::getenv("HBEM_SKIP_NEARFIELD") != nullptr;  // timing experiments only
+  if (H->D.n_spairs > 0 && !skip_nf) {
     HB_CHECK((sing_table_launch<T, C>(P, H->D, ctx->op, ctx->helm, nt, ns, H->side)));
     ++launches;
   }
   HB_CUDA(cudaEventRecord(H->tab_done, H->side));
   if (!H->p0) HB_CUDA(cudaStreamWaitEvent(st, H->tab_done, 0));  // k_aca_gen reads the table
-  if (H->nd > 0) {
+  if (H->nd > 0 && !skip_nf) {
     HB_CUDA(cudaMemsetAsync(H->D.sing_count, 0, 8, H->side));
     HB_CUDA(cudaMemsetAsync(H->D.stat, 0, 16, H->side));
     if (H->p0) {

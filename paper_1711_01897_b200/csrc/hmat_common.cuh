@@ -144,6 +144,42 @@ template <typename T> struct Prob {
   const void *stab;
 };
 
+// Point kernel of kernel_planes (kernels.py:129-158) for d = x - y:
+// SLP 1/r, DLP <d, n_y>/r^3, ADLP -<d, n_x>/r^3, Helmholtz factors e^{ikr}
+// (SLP) and (cos kr + kr sin kr, sin kr - kr cos kr) (DLP/ADLP); 1/(4 pi)
+// is applied by the caller.  nt / nf: normal of the test / trial element.
+template <typename T, int OP, bool HELM>
+__device__ __forceinline__ void point_kernel(const RuleTab<T> &R, T d0, T d1, T d2,
+                                             const T *ntest, const T *ntrial, T &gr, T &gi) {
+  const T r2 = d0 * d0 + d1 * d1 + d2 * d2;
+  const T ri = rsqrt_t<T>(r2);
+  gi = T(0);
+  if (OP == HBEM_SLP) {
+    if (!HELM) {
+      gr = ri;
+    } else {
+      const T kr = R.k * (r2 * ri);
+      T s, c;
+      sincos_t<T>(kr, &s, &c);
+      gr = ri * c;
+      gi = ri * s;
+    }
+  } else {
+    const T dot = OP == HBEM_DLP ? d0 * ntrial[0] + d1 * ntrial[1] + d2 * ntrial[2]
+                                 : -(d0 * ntest[0] + d1 * ntest[1] + d2 * ntest[2]);
+    const T amp = dot * (ri * ri * ri);
+    if (!HELM) {
+      gr = amp;
+    } else {
+      const T kr = R.k * (r2 * ri);
+      T s, c;
+      sincos_t<T>(kr, &s, &c);
+      gr = amp * (c + kr * s);
+      gi = amp * (s - kr * c);
+    }
+  }
+}
+
 // block of one element pair (any adjacency), thread-level
 template <typename T, int OP, bool HELM, int NT, int NS>
 __device__ __forceinline__ void pair_block(const Prob<T> &P, int e, int f, T (&re)[NT][NS],
@@ -203,9 +239,41 @@ __device__ __forceinline__ typename Num<T, C>::V entry(const Prob<T> &P, int di,
   for (int t = t0; t < t1; ++t) {
     const int e = NT == 1 ? di : P.tel[t];
     const int a = NT == 1 ? 0 : P.tloc[t];
+    T x[18], na[4];
+    if (OP != HBEM_HYPS) {
+      load_q<T>(P.g.q, e, x);
+      load_nj<T>(P.g.nj, e, na);
+    }
     for (int s = s0; s < s1; ++s) {
       const int f = NS == 1 ? dj : P.sel[s];
       const int b = NS == 1 ? 0 : P.sloc[s];
+      if (OP != HBEM_HYPS && !touching(P.elem[e], P.elem[f])) {
+        // only the (a, b) basis pair of the block is needed: one weighted
+        // accumulation per quadrature-point pair instead of the 3 x 3 block
+        T y[18], nb[4];
+        load_q<T>(P.g.q, f, y);
+        load_nj<T>(P.g.nj, f, nb);
+        T sr = T(0), si = T(0);
+#pragma unroll
+        for (int pp = 0; pp < 6; ++pp) {
+          T ar = T(0), ai = T(0);
+#pragma unroll
+          for (int qq = 0; qq < 6; ++qq) {
+            T gr, gi;
+            point_kernel<T, OP, HELM>(P.R, x[3 * pp] - y[3 * qq], x[3 * pp + 1] - y[3 * qq + 1],
+                                      x[3 * pp + 2] - y[3 * qq + 2], na, nb, gr, gi);
+            ar += P.R.wb[b][qq] * gr;
+            if (HELM) ai += P.R.wb[b][qq] * gi;
+          }
+          sr += P.R.wa[a][pp] * ar;
+          if (HELM) si += P.R.wa[a][pp] * ai;
+        }
+        const T scale = (na[3] * nb[3]) * T(kInv4Pi);
+        const typename N::V val = N::mk(scale * sr, HELM ? scale * si : T(0));
+        if constexpr (C) { acc.re += val.re; acc.im += val.im; }
+        else acc += val;
+        continue;
+      }
       T re[NT][NS], im[NT][NS];
       pair_block<T, OP, HELM, NT, NS>(P, e, f, re, im, nsing);
       T vr = T(0), vi = T(0);
@@ -230,42 +298,6 @@ __device__ __forceinline__ typename Num<T, C>::V p0_regular(const RuleTab<T> &R,
   T re[1][1], im[1][1];
   regular_pair<T, OP, HELM, 1, 1>(R, x, y, na, nb, nullptr, nullptr, re, im);
   return Num<T, C>::mk(re[0][0], im[0][0]);
-}
-
-// Point kernel of kernel_planes (kernels.py:129-158) for d = x - y:
-// SLP 1/r, DLP <d, n_y>/r^3, ADLP -<d, n_x>/r^3, Helmholtz factors e^{ikr}
-// (SLP) and (cos kr + kr sin kr, sin kr - kr cos kr) (DLP/ADLP); 1/(4 pi)
-// is applied by the caller.  nt / nf: normal of the test / trial element.
-template <typename T, int OP, bool HELM>
-__device__ __forceinline__ void point_kernel(const RuleTab<T> &R, T d0, T d1, T d2,
-                                             const T *ntest, const T *ntrial, T &gr, T &gi) {
-  const T r2 = d0 * d0 + d1 * d1 + d2 * d2;
-  const T ri = rsqrt_t<T>(r2);
-  gi = T(0);
-  if (OP == HBEM_SLP) {
-    if (!HELM) {
-      gr = ri;
-    } else {
-      const T kr = R.k * (r2 * ri);
-      T s, c;
-      sincos_t<T>(kr, &s, &c);
-      gr = ri * c;
-      gi = ri * s;
-    }
-  } else {
-    const T dot = OP == HBEM_DLP ? d0 * ntrial[0] + d1 * ntrial[1] + d2 * ntrial[2]
-                                 : -(d0 * ntest[0] + d1 * ntest[1] + d2 * ntest[2]);
-    const T amp = dot * (ri * ri * ri);
-    if (!HELM) {
-      gr = amp;
-    } else {
-      const T kr = R.k * (r2 * ri);
-      T s, c;
-      sincos_t<T>(kr, &s, &c);
-      gr = amp * (c + kr * s);
-      gi = amp * (s - kr * c);
-    }
-  }
 }
 
 // Regular P0 pairs of NJ fixed elements (points read from shared memory in
