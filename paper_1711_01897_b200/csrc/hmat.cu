@@ -1057,7 +1057,6 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
     HB_CHECK((emit_converged<T, C>(H, st, /*pack=*/false)));
   }
   H->packed = H->streaming();
-  HB_CUDA(cudaStreamWaitEvent(st, H->tab_done, 0));  // fallback rows may read the table
   const auto t_aca = clk::now();
   // ---- classify admissible blocks (lowrank_leaf, hmatrix.py:721-735) -------------
   std::vector<int> st_h(na), rk_h(na), ex_h(na);
@@ -1189,6 +1188,7 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
       HB_CHECK(dalloc_tmp(H, &F.sing_pos, ent));
     }
     const unsigned ntl = (unsigned)tslot.size();
+    HB_CUDA(cudaStreamWaitEvent(st, H->tab_done, 0));  // exact rows may read the table
     int rc = dispatch_op(ctx->op, ctx->helm, nt, ns, [&](auto OPc, auto Hc, auto NTc,
                                                          auto NSc) -> int {
       constexpr int OP = decltype(OPc)::value;

@@ -320,7 +320,7 @@ __device__ __forceinline__ void p0_pairs_fx(const RuleTab<T> &R, const ElemRec<T
     T ar[NJ], ai[NJ];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) { ar[j] = T(0); ai[j] = T(0); }
-#pragma unroll(NJ == 1 ? 2 : kInnerUnroll2)
+#pragma unroll(NJ == 1 ? 2 : (HELM ? 2 : kInnerUnroll2))
     for (int o = 0; o < 6; ++o) {
       const T wo = FIXED_TEST ? R.wa[0][o] : R.wb[0][o];
 #pragma unroll
