@@ -73,11 +73,11 @@ static __global__ void k_phase_flags(const unsigned char *flag, const int *order
 }
 
 template <int NC>
-__global__ void k_need(AcaDev S, int na, int col) {
+__global__ void k_need(AcaDev S, int na, int col, int NT_, int NS_) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= na) return;
   const int n = *S.nlist;
-  Need d{0, 0, 0};
+  Need d{0, 0, 0, 0, 0};
   if (p < n) {
     const int b = S.list[p];
     const int h = S.h[b], w = S.w[b], k = S.rank[b];
@@ -93,6 +93,13 @@ __global__ void k_need(AcaDev S, int na, int col) {
     // job's records start 16-byte aligned
     d.part = ((long long)tiles * k * NC + 1) & ~1ll;
     d.items = head ? tiles : 0;
+    if (NT_ != 1 || NS_ != 1) {
+      // element-level rows: the varying cluster's element union
+      const long long *ep = col ? S.recl_ptr : S.cecl_ptr;
+      const long long ne = ep[key + 1] - ep[key];
+      d.eitems = head ? (ne + 31) / 32 : 0;
+      d.rsc = ne * (col ? NT_ : NS_);
+    }
   }
   S.need[p] = d;
 }
@@ -112,6 +119,7 @@ __global__ void k_jobs(AcaDev S, int n, int col) {
   J.k = S.rank[b];
   const int r0 = S.r0[b], c0 = S.c0[b];
   J.part = sc.part - nd.part;
+  J.rsc = sc.rsc - nd.rsc;
   if (!col) {
     J.key = S.cnode[b];
     J.fix = S.cur[b];
@@ -151,6 +159,10 @@ __global__ void k_jobs(AcaDev S, int n, int col) {
   if (nd.items) {
     const long long base = sc.items - nd.items;
     for (long long t = 0; t < nd.items; ++t) S.items[base + t] = make_int2(p, (int)t);
+  }
+  if (nd.eitems) {
+    const long long base = sc.eitems - nd.eitems;
+    for (long long t = 0; t < nd.eitems; ++t) S.eitems[base + t] = make_int2(p, (int)t);
   }
 }
 
@@ -227,6 +239,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 struct JobS {
   long long pe;     // pending record
   long long part;   // first tile record
+  long long rsc_off;  // element-row values (linear spaces)
   long long mofs;   // mask word base of the varying side
   int b, h, w, k, fix, cur;
 };
@@ -308,6 +321,7 @@ __device__ __forceinline__ bool stage_job(const AcaDev &S, int p, int n, int key
   if (J.key != key0) return false;
   js.pe = J.pe;
   js.part = J.part;
+  js.rsc_off = J.rsc;
   js.mofs = COL ? S.rmask_off[J.b] : S.cmask_off[J.b];
   js.b = J.b;
   js.h = J.h;
@@ -453,6 +467,142 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
   }
 }
 
+// ---------------------------------------------------------------------------
+// K3e (linear spaces, element level): one warp per (group head, 32-element
+// tile of the varying cluster's element union).  Lane l keeps element h of
+// the union in registers; for every job of the group the fixed DOF's
+// elements g (local basis a_g) are staged in shared memory and the lane
+// accumulates the row (row phase: trial basis b of h) or column (column
+// phase: test basis a of h) of sum_g B_gh[a_g, .] — every element pair is
+// integrated once with all NL basis functions of the lane element sharing
+// each kernel evaluation (the reference's pairs = repeat(T(dof)) x
+// tile(col_elems), hmatrix.py:636-639).  Touching pairs read the singular
+// table.  k_aca_gen then gathers DOF entries from these rows.
+// ---------------------------------------------------------------------------
+template <typename T, bool C, int OP, bool HELM, int NT, int NS, bool COL>
+__global__ void __launch_bounds__(kThreads) k_p1_erow(Prob<T> P, AcaDev S, int n,
+                                                      long long n_items) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  constexpr int NL = COL ? NT : NS;  // basis functions of the lane element
+  constexpr int KE = 16;             // fixed elements staged per chunk
+  __shared__ T sq[kWarps][KE][18];
+  __shared__ T snj[kWarps][KE][4];
+  __shared__ int4 sev[kWarps][KE];
+  __shared__ int sloc[kWarps][KE];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long item = (long long)blockIdx.x * kWarps + wid;
+  if (item >= n_items) return;
+  const int2 it = S.eitems[item];
+  const int p0 = it.x, te = it.y;
+  const int key0 = S.jobs[p0].key;
+  const long long *ep = COL ? S.recl_ptr : S.cecl_ptr;
+  const int *el = COL ? S.recl : S.cecl;
+  const long long e0 = ep[key0], ne = ep[key0 + 1] - e0;
+  const long long li = (long long)te * 32 + lane;
+  const bool valid = li < ne;
+  const int h = el[e0 + (valid ? li : 0)];
+  T y[18], nl[4];
+  load_q<T>(P.g.q, h, y);
+  load_nj<T>(P.g.nj, h, nl);
+  int4 hev = P.elem[h];
+  hev.w = h;
+  const int *fptr = COL ? P.sptr : P.tptr;
+  const int *fel = COL ? P.sel : P.tel;
+  const signed char *floc = COL ? P.sloc : P.tloc;
+  const int *fperm = COL ? P.cperm : P.rperm;
+  V *out = static_cast<V *>(S.rsc);
+  for (int p = p0; p < n; ++p) {
+    const Job J = S.jobs[p];
+    if (J.key != key0) break;
+    const int dof = fperm[J.nfix];
+    constexpr bool kFixedP0 = (COL ? NS : NT) == 1;  // fixed DOF = its element
+    const int f0 = kFixedP0 ? 0 : fptr[dof], f1 = kFixedP0 ? 1 : fptr[dof + 1];
+    T rr[NL], ri[NL];
+#pragma unroll
+    for (int b = 0; b < NL; ++b) { rr[b] = T(0); ri[b] = T(0); }
+    for (int c0 = f0; c0 < f1; c0 += KE) {
+      const int cnt = min(KE, f1 - c0);
+      if (lane < cnt) {
+        const int g = kFixedP0 ? dof : fel[c0 + lane];
+        T q[18], nj[4];
+        load_q<T>(P.g.q, g, q);
+        load_nj<T>(P.g.nj, g, nj);
+#pragma unroll
+        for (int c = 0; c < 18; ++c) sq[wid][lane][c] = q[c];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) snj[wid][lane][c] = nj[c];
+        int4 ev = P.elem[g];
+        ev.w = g;
+        sev[wid][lane] = ev;
+        sloc[wid][lane] = kFixedP0 ? 0 : floc[c0 + lane];
+      }
+      __syncwarp();
+      for (int k = 0; k < cnt; ++k) {
+        const int4 gev = sev[wid][k];
+        const int a = sloc[wid][k];
+        if (touching4(gev, hev)) {
+          if (valid) {
+            // table block of (test, trial): row phase (g, h), column (h, g)
+            const int et = COL ? h : gev.w, ft = COL ? gev.w : h;
+            int j = P.nb_ptr[et];
+            while (P.nb_idx[j] != ft) ++j;
+            const T *blk = static_cast<const T *>(P.stab) + (long long)j * NT * NS * (HELM ? 2 : 1);
+#pragma unroll
+            for (int b = 0; b < NL; ++b) {
+              const int o = COL ? b * NS + a : a * NS + b;
+              rr[b] += HELM ? blk[2 * o] : blk[o];
+              if (HELM) ri[b] += blk[2 * o + 1];
+            }
+            atomicAdd(S.stat + 1, 1ull);
+          }
+          continue;
+        }
+        // regular pair: lane points outer, fixed points inner
+        T sr[NL], si[NL];
+#pragma unroll
+        for (int b = 0; b < NL; ++b) { sr[b] = T(0); si[b] = T(0); }
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const T y0 = y[3 * i], y1 = y[3 * i + 1], y2 = y[3 * i + 2];
+          T tr = T(0), ti = T(0);
+#pragma unroll 2
+          for (int o = 0; o < 6; ++o) {
+            const T g0 = sq[wid][k][3 * o], g1 = sq[wid][k][3 * o + 1], g2 = sq[wid][k][3 * o + 2];
+            T gr, gi;
+            // d = x - y with x the test point
+            if (!COL)
+              point_kernel<T, OP, HELM>(P.R, g0 - y0, g1 - y1, g2 - y2, snj[wid][k], nl, gr, gi);
+            else
+              point_kernel<T, OP, HELM>(P.R, y0 - g0, y1 - g1, y2 - g2, nl, snj[wid][k], gr, gi);
+            const T wf = COL ? P.R.wb[a][o] : P.R.wa[a][o];
+            tr += wf * gr;
+            if (HELM) ti += wf * gi;
+          }
+#pragma unroll
+          for (int b = 0; b < NL; ++b) {
+            const T wl = COL ? P.R.wa[b][i] : P.R.wb[b][i];
+            sr[b] += wl * tr;
+            if (HELM) si[b] += wl * ti;
+          }
+        }
+        const T scale = (snj[wid][k][3] * nl[3]) * T(kInv4Pi);
+#pragma unroll
+        for (int b = 0; b < NL; ++b) {
+          rr[b] += scale * sr[b];
+          if (HELM) ri[b] += scale * si[b];
+        }
+      }
+      __syncwarp();
+    }
+    if (valid) {
+      V *o = out + J.rsc + li * NL;
+#pragma unroll
+      for (int b = 0; b < NL; ++b) o[b] = N::mk(rr[b], ri[b]);
+    }
+  }
+}
+
 // K3 (linear spaces): entries summed over the carrying element pairs
 template <typename T, bool C, int OP, bool HELM, int NT, int NS, bool COL>
 __global__ void __launch_bounds__(kThreads) k_aca_gen(Prob<T> P, AcaDev S, int n,
@@ -499,9 +649,38 @@ __global__ void __launch_bounds__(kThreads) k_aca_gen(Prob<T> P, AcaDev S, int n
       if (l < kk && valid) cp_async<sizeof(V)>(&fbuf[wid][l * 32 + lane], pool + gjt[l] + ro + idx);
     const int fdof = COL ? P.cperm[S.c0[J.b] + J.fix] : P.rperm[S.r0[J.b] + J.fix];
     V val = N::zero();
-    if (valid)
+    if (OP != HBEM_HYPS && S.rsc) {
+      // element rows (k_p1_erow): entry = sum over the varying DOF's elements
+      // of their row value at the DOF's local basis function, elements in
+      // ascending order (the order of _row_job / _col_job's scatter)
+      if (valid) {
+        constexpr int NL = COL ? NT : NS;
+        const long long *ep = COL ? S.recl_ptr : S.cecl_ptr;
+        const int *el = COL ? S.recl : S.cecl;
+        const long long e0 = ep[key0], e1 = ep[key0 + 1];
+        const int *iptr = COL ? P.tptr : P.sptr;
+        const int *iel = COL ? P.tel : P.sel;
+        const signed char *iloc = COL ? P.tloc : P.sloc;
+        const V *R = static_cast<const V *>(S.rsc) + J.rsc_off;
+        constexpr bool kVarP0 = NL == 1;  // varying DOF = its element
+        const int q0 = kVarP0 ? 0 : iptr[vdof], q1 = kVarP0 ? 1 : iptr[vdof + 1];
+        for (int q = q0; q < q1; ++q) {
+          const int f = kVarP0 ? vdof : iel[q];
+          long long lo = e0, hi = e1;
+          while (lo < hi) {
+            const long long mid = (lo + hi) >> 1;
+            if (el[mid] < f) lo = mid + 1;
+            else hi = mid;
+          }
+          const V r = R[(lo - e0) * NL + (kVarP0 ? 0 : iloc[q])];
+          if constexpr (C) { val.re += r.re; val.im += r.im; }
+          else val += r;
+        }
+      }
+    } else if (valid) {
       val = COL ? entry<T, C, OP, HELM, NT, NS>(P, vdof, fdof, S.stat + 1)
                 : entry<T, C, OP, HELM, NT, NS>(P, fdof, vdof, S.stat + 1);
+    }
     cp_async_wait_all();
     aca_epi<T, C, COL>(S, J, sjc[wid], t, lane, valid, val, fbuf[wid]);
     nent += valid ? 1 : 0;
@@ -760,7 +939,7 @@ int aca_select(const Prob<T> &, AcaDev &S, const PhaseArgs &A, cudaStream_t st) 
     HB_CUDA(cudaMemsetAsync(S.flagA, 0, na, st));
     HB_CUDA(cudaMemsetAsync(S.flagC, 0, na, st));
   }
-  k_need<NC><<<(na + 255) / 256, 256, 0, st>>>(S, na, A.col_phase);
+  k_need<NC><<<(na + 255) / 256, 256, 0, st>>>(S, na, A.col_phase, A.nt, A.ns);
   HB_CUDA(cudaGetLastError());
   tb = A.cub_bytes;
   HB_CUDA(cub::DeviceScan::InclusiveScan(A.cub_tmp, tb, S.need, S.scan, SumNeed(), na, st));
@@ -778,11 +957,29 @@ inline size_t aca_cub_bytes_impl(int na) {
 
 template <typename T, bool C>
 int aca_phase(const Prob<T> &P, AcaDev &S, const PhaseArgs &A, int op, bool helm, int nt, int ns,
-              int n, long long n_items, cudaStream_t st) {
+              int n, long long n_items, long long n_eitems, cudaStream_t st) {
   if (n <= 0) return HBEM_OK;
   const int col = A.col_phase;
   k_jobs<T, C><<<(n + 127) / 128, 128, 0, st>>>(S, n, col);
   HB_CUDA(cudaGetLastError());
+  if (S.rsc && n_eitems > 0) {
+    // linear spaces: element rows first, then the DOF gather + residual
+    const unsigned egrid = (unsigned)((n_eitems + kWarps - 1) / kWarps);
+    int rc = dispatch_op(op, helm, nt, ns, [&](auto OPc, auto Hc, auto NTc, auto NSc) -> int {
+      constexpr int OP = decltype(OPc)::value;
+      constexpr bool HH = decltype(Hc)::value != 0;
+      constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
+      if constexpr (HH == C && (NT != 1 || NS != 1) && OP != HBEM_HYPS) {
+        if (col) k_p1_erow<T, C, OP, HH, NT, NS, true><<<egrid, kThreads, 0, st>>>(P, S, n, n_eitems);
+        else k_p1_erow<T, C, OP, HH, NT, NS, false><<<egrid, kThreads, 0, st>>>(P, S, n, n_eitems);
+        HB_CUDA(cudaGetLastError());
+        return HBEM_OK;
+      } else {
+        return set_error(HBEM_ERR_KERNEL, "element rows requested for an unsupported operator");
+      }
+    });
+    if (rc != HBEM_OK) return rc;
+  }
   if (n_items > 0) {
     const unsigned grid = (unsigned)((n_items + kWarps - 1) / kWarps);
     if (A.int_beg) HB_CUDA(cudaEventRecord(A.int_beg, st));

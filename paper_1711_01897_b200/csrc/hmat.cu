@@ -319,6 +319,10 @@ struct hbem_hmat {
   double *partA = nullptr, *partC = nullptr;
   size_t partA_cap = 0, partC_cap = 0;  // doubles
   long long items_cap = 0;
+  bool use_erows = false;       // linear spaces: element-level ACA rows
+  long long eitems_cap = 0;
+  void *rsc = nullptr;          // element-row values of the current phase
+  size_t rsc_cap = 0;           // bytes
   AcaDev S{};
   VPool vpool;  // ACA factor pool
   Geo64 *g64p = nullptr;  // device copy of the context's float64 geometry view
@@ -383,6 +387,7 @@ struct hbem_hmat {
     cudaFree(dense_adm);
     cudaFree(partA);
     cudaFree(partC);
+    cudaFree(rsc);
     cudaFree(mv_buf);
     cudaFree(mv_lr);
     cudaFree(mv_ad);
@@ -561,8 +566,10 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
     H->trec = t;
     H->srec = s;
   }
+  Incidence tinc, sinc;  // host copies (linear spaces): element unions per cluster
   if (nt == 3) {
     Incidence I = incidence(d->test_dofmap, m, 3, d->n_rows);
+    tinc = I;
     int *p, *e;
     signed char *l;
     HB_CHECK(upload(H, &p, I.ptr));
@@ -572,6 +579,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   }
   if (ns == 3) {
     Incidence I = incidence(d->trial_dofmap, m, 3, d->n_cols);
+    sinc = I;
     int *p, *e;
     signed char *l;
     HB_CHECK(upload(H, &p, I.ptr));
@@ -614,6 +622,65 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
     max_items += std::max(tiles_of(h), tiles_of(w));
   }
   H->items_cap = std::max<long long>(max_items, 1);
+  // ---- linear spaces: sorted element union per cluster node (row and column
+  // tree), the varying side of the element-level ACA rows (k_p1_erow)
+  H->use_erows = !H->p0 && ctx->op != HBEM_HYPS;
+  if (H->use_erows) {
+    auto unions = [&](const int64_t *nodes, int64_t n_nodes, const int64_t *perm,
+                      const Incidence &inc, bool single, long long **dptr, int **del,
+                      long long &tiles) -> int {
+      std::vector<long long> ptr(n_nodes + 1, 0);
+      std::vector<std::vector<int>> lists(n_nodes);
+      // bottom-up where children follow their parent, direct otherwise
+      for (int64_t q = n_nodes - 1; q >= 0; --q) {
+        const int64_t l = nodes[5 * q + 3], r = nodes[5 * q + 4];
+        std::vector<int> &E = lists[q];
+        if (l > q && r > q && l < n_nodes && r < n_nodes) {
+          E.resize(lists[l].size() + lists[r].size());
+          auto it = std::set_union(lists[l].begin(), lists[l].end(), lists[r].begin(),
+                                   lists[r].end(), E.begin());
+          E.resize(it - E.begin());
+        } else {
+          for (int64_t tp = nodes[5 * q]; tp < nodes[5 * q + 1]; ++tp) {
+            const int64_t dof = perm[tp];
+            if (single) {
+              E.push_back((int)dof);
+            } else {
+              for (int k = inc.ptr[dof]; k < inc.ptr[dof + 1]; ++k) E.push_back(inc.el[k]);
+            }
+          }
+          std::sort(E.begin(), E.end());
+          E.erase(std::unique(E.begin(), E.end()), E.end());
+        }
+      }
+      for (int64_t q = 0; q < n_nodes; ++q) {
+        ptr[q + 1] = ptr[q] + (long long)lists[q].size();
+        tiles += ((long long)lists[q].size() + 31) / 32;
+      }
+      std::vector<int> flat(ptr[n_nodes]);
+      for (int64_t q = 0; q < n_nodes; ++q)
+        std::copy(lists[q].begin(), lists[q].end(), flat.begin() + ptr[q]);
+      HB_CHECK(upload(H, dptr, ptr));
+      HB_CHECK(upload(H, del, flat));
+      return HBEM_OK;
+    };
+    long long et = 0;
+    long long *rp = nullptr, *cpp = nullptr;
+    int *re = nullptr, *ce = nullptr;
+    HB_CHECK(unions(d->row_nodes, d->n_row_nodes, d->row_perm, tinc, nt == 1, &rp, &re, et));
+    if (H->same_tree && nt == ns) {
+      cpp = rp;
+      ce = re;
+      et *= 2;
+    } else {
+      HB_CHECK(unions(d->col_nodes, d->n_col_nodes, d->col_perm, sinc, ns == 1, &cpp, &ce, et));
+    }
+    H->S.recl_ptr = rp;
+    H->S.recl = re;
+    H->S.cecl_ptr = cpp;
+    H->S.cecl = ce;
+    H->eitems_cap = std::max<long long>(et, 1);
+  }
   AcaDev &S = H->S;
   int tmax = d->rank_capacity > 0 ? d->rank_capacity : 64;
   S.tmax = std::min(tmax, 256);
@@ -669,6 +736,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   HB_CHECK(dalloc(H, &S.jt, (size_t)na * kFinRegs));
   HB_CHECK(dalloc(H, (char **)&S.jc, (size_t)na * kFinRegs * H->vbytes));
   HB_CHECK(dalloc(H, &S.items, H->items_cap));
+  if (H->use_erows) HB_CHECK(dalloc(H, &S.eitems, H->eitems_cap));
   HB_CHECK(dalloc(H, &S.stat, 4));
   H->cub_bytes = aca_cub_bytes(na);
   HB_CHECK(dalloc(H, (char **)&H->cub_tmp, H->cub_bytes));
@@ -837,6 +905,8 @@ int run_phase(hbem_hmat *H, const Prob<T> &P, int col, long long &pool_top, int 
   A.cub_tmp = H->cub_tmp;
   A.cub_bytes = H->cub_bytes;
   A.sel_tmp = H->sel_tmp;
+  A.nt = H->nt;
+  A.ns = H->ns;
   S.list = col ? H->listC : H->listA;
   S.nlist = H->d_cnt;
   HB_CHECK((aca_select<T, C>(P, S, A, st)));
@@ -871,7 +941,28 @@ int run_phase(hbem_hmat *H, const Prob<T> &P, int col, long long &pool_top, int 
   A.int_beg = H->iev[col][0];
   A.int_end = H->iev[col][1];
   H->int_pending[col] = tot.items > 0;
-  return aca_phase<T, C>(P, S, A, ctx->op, ctx->helm, H->nt, H->ns, n, tot.items, st);
+  S.rsc = nullptr;
+  if (H->use_erows) {
+    if (tot.eitems > H->eitems_cap)
+      return set_error(HBEM_ERR_CAPACITY, "element item table overflow (%lld > %lld)",
+                       (long long)tot.eitems, (long long)H->eitems_cap);
+    const size_t need = (size_t)std::max<long long>(tot.rsc, 1) * H->vbytes;
+    if (need > H->rsc_cap) {
+      cudaFree(H->rsc);
+      H->rsc = nullptr;
+      const size_t cap = need + need / 4;
+      cudaError_t e = cudaMalloc(&H->rsc, cap);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        H->rsc_cap = 0;
+        return set_error(HBEM_ERR_CAPACITY, "element-row scratch of %zu bytes: %s", cap,
+                         cudaGetErrorString(e));
+      }
+      H->rsc_cap = cap;
+    }
+    S.rsc = H->rsc;
+  }
+  return aca_phase<T, C>(P, S, A, ctx->op, ctx->helm, H->nt, H->ns, n, tot.items, tot.eitems, st);
 }
 
 // pack the low-rank blocks converged since the last call into the device

@@ -420,6 +420,7 @@ struct Job {
   int cur;          // column phase: the block's current row i (excluded from the next pivot)
   long long pe;     // pool record of the pending term [u (h) | v (w)]
   long long part;   // first partial record of this job (doubles)
+  long long rsc;    // linear spaces: element-row values of this job (V units)
 };
 
 // partial record per (job, 32-wide tile): best |val| over unmasked entries,
@@ -431,12 +432,16 @@ __host__ __device__ __forceinline__ long long part_len(int k, int nc) { return 4
 __host__ __device__ __forceinline__ long long part_dots(int nt) { return 4ll * nt; }
 __host__ __device__ __forceinline__ int tiles_of(int n) { return (n + 31) >> 5; }
 
-struct Need {  // per-position allocation need (pool values, partial doubles, items)
-  long long pool, part, items;
+// per-position allocation need: pool values, dot-record doubles, DOF-tile warp
+// items, element-tile warp items (linear spaces) and element-row values
+// (linear spaces: NT or NS per element of the varying cluster's union)
+struct Need {
+  long long pool, part, items, eitems, rsc;
 };
 struct SumNeed {
   __device__ __forceinline__ Need operator()(const Need &a, const Need &b) const {
-    return Need{a.pool + b.pool, a.part + b.part, a.items + b.items};
+    return Need{a.pool + b.pool, a.part + b.part, a.items + b.items, a.eitems + b.eitems,
+                a.rsc + b.rsc};
   }
 };
 
@@ -462,6 +467,12 @@ struct AcaDev {
   Need *need, *scan;
   Job *jobs;
   int2 *items;       // (head position, tile)
+  int2 *eitems;      // linear spaces: (head position, element tile)
+  void *rsc;         // linear spaces: element-row values of the current phase
+  // linear spaces: per cluster node, the sorted union of the elements that
+  // carry its DOFs (row tree / column tree CSR)
+  const long long *recl_ptr, *cecl_ptr;
+  const int *recl, *cecl;
   double *part;      // dot records of the current phase (k values per job)
   long long *jt;     // per job: record offsets of its first kFinRegs terms
   void *jc;          // per job: their residual coefficients (u_l[i] / p_l or r_l[j] / p_l)
@@ -512,6 +523,7 @@ struct PhaseArgs {
   void *cub_tmp;
   size_t cub_bytes;
   int *sel_tmp;       // na flags scratch for the compaction
+  int nt, ns;         // basis functions per element (test, trial)
   cudaEvent_t int_beg, int_end;  // recorded around the integration launch (may be null)
 };
 
@@ -523,7 +535,7 @@ int aca_select(const Prob<T> &P, AcaDev &S, const PhaseArgs &A, cudaStream_t st)
 // jobs + items + integration + finalize for a phase of n jobs and n_items items
 template <typename T, bool C>
 int aca_phase(const Prob<T> &P, AcaDev &S, const PhaseArgs &A, int op, bool helm, int nt, int ns,
-              int n, long long n_items, cudaStream_t st);
+              int n, long long n_items, long long n_eitems, cudaStream_t st);
 size_t aca_cub_bytes(int na);
 
 template <typename T>

@@ -12,9 +12,9 @@ template int aca_select<float, false>(const Prob<float> &, AcaDev &, const Phase
 template int aca_select<float, true>(const Prob<float> &, AcaDev &, const PhaseArgs &,
                                       cudaStream_t);
 template int aca_phase<float, false>(const Prob<float> &, AcaDev &, const PhaseArgs &, int, bool,
-                                      int, int, int, long long, cudaStream_t);
+                                      int, int, int, long long, long long, cudaStream_t);
 template int aca_phase<float, true>(const Prob<float> &, AcaDev &, const PhaseArgs &, int, bool,
-                                     int, int, int, long long, cudaStream_t);
+                                     int, int, int, long long, long long, cudaStream_t);
 template int near_p0_launch<float, false>(const Prob<float> &, const DenseDev &, int, bool,
                                            cudaStream_t);
 template int near_p0_launch<float, true>(const Prob<float> &, const DenseDev &, int, bool,

@@ -13,9 +13,9 @@ template int aca_select<double, false>(const Prob<double> &, AcaDev &, const Pha
 template int aca_select<double, true>(const Prob<double> &, AcaDev &, const PhaseArgs &,
                                       cudaStream_t);
 template int aca_phase<double, false>(const Prob<double> &, AcaDev &, const PhaseArgs &, int, bool,
-                                      int, int, int, long long, cudaStream_t);
+                                      int, int, int, long long, long long, cudaStream_t);
 template int aca_phase<double, true>(const Prob<double> &, AcaDev &, const PhaseArgs &, int, bool,
-                                     int, int, int, long long, cudaStream_t);
+                                     int, int, int, long long, long long, cudaStream_t);
 template int near_p0_launch<double, false>(const Prob<double> &, const DenseDev &, int, bool,
                                            cudaStream_t);
 template int near_p0_launch<double, true>(const Prob<double> &, const DenseDev &, int, bool,
