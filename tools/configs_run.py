@@ -47,6 +47,8 @@ def configs():
     k4 = 2 * np.pi / (8 * h_max(v, e))         # ~8 elements per wavelength
     out.append(("C4-dlp-p1c-f32", v, e, "p1c", "helmholtz", "dlp", k4, 1e-3, "single"))
     out.append(("C4-slp-p0-f64", v, e, "p0", "helmholtz", "slp", k4, 1e-3, "double"))
+    # combined field (scatter.py:270-306): Helmholtz SLP on P1d, 3 DOFs per element
+    out.append(("C4-slp-p1d-f32", v, e, "p1d", "helmholtz", "slp", k4, 1e-3, "single"))
     return out
 
 
