@@ -429,6 +429,8 @@ def run_ours(args):
                 "pairs_per_step": {"regular": int((pairs - sing) / args.steps),
                                    "singular": int(sing / args.steps)},
                 "aca": {"waves": stats["waves"], "row_jobs": stats["row_jobs"],
+                        "host_wall_s": {"waves": stats["seconds_aca"],
+                                        "classify_expand_copyback": stats["seconds_finalize"]},
                         "lowrank_leaves": stats["lowrank_leaves"],
                         "dense_leaves": stats["dense_leaves"],
                         "stored_entries": stats["u_entries"] + stats["v_entries"]

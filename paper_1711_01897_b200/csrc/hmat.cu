@@ -180,6 +180,70 @@ __global__ void k_emit_offsets(const int *list, int n, const longlong2 *scan,
   q_voff[p] = vo;
 }
 
+// classification of every admissible block after the waves (lowrank_leaf /
+// dense fallback, hmatrix.py:721-735), on the device: per-leaf metadata
+// written in place (kind, rank, flags | off_u, off_v, off_dense), dense sizes
+// for the offset scan, low-rank / dense flags for the two block lists
+struct LeafMeta {
+  int *kind, *rank, *flags;           // L each
+  long long *off_u, *off_v, *off_d;   // L each
+};
+
+struct ClsStat {
+  unsigned long long converged, exhausted;
+  int overflow_q, pad;
+};
+
+__global__ void k_classify(AcaDev S, int na, const int *adm_leaf, const long long *blk_uoff,
+                           const long long *blk_voff, LeafMeta M, longlong2 *dsz,
+                           unsigned char *flag_lr, unsigned char *flag_dn, ClsStat *cs) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  bool conv = false, exh = false;
+  if (q < na) {
+    const int s = S.status[q];
+    const long long h = S.h[q], w = S.w[q], k = S.rank[q];
+    conv = s == ST_CONVERGED;
+    exh = S.exhausted[q] != 0;
+    if (s == ST_OVERFLOW) atomicMin(&cs->overflow_q, q);
+    const bool lr = conv && k * (h + w) < h * w;
+    const int lf = adm_leaf[q];
+    M.kind[lf] = lr ? 1 : 0;
+    M.rank[lf] = (int)k;
+    M.flags[lf] = (conv ? 1 : 0) | (exh ? 2 : 0);
+    M.off_u[lf] = lr ? blk_uoff[q] : -1;
+    M.off_v[lf] = lr ? blk_voff[q] : -1;
+    if (lr) M.off_d[lf] = -1;  // dense offsets after the scan
+    dsz[q] = make_longlong2(lr ? 0 : h * w, 0);
+    flag_lr[q] = lr ? 1 : 0;
+    flag_dn[q] = lr ? 0 : 1;
+  }
+  const unsigned nc = __popc(__ballot_sync(0xffffffffu, conv));
+  const unsigned ne = __popc(__ballot_sync(0xffffffffu, exh));
+  if ((threadIdx.x & 31) == 0) {
+    if (nc) atomicAdd(&cs->converged, (unsigned long long)nc);
+    if (ne) atomicAdd(&cs->exhausted, (unsigned long long)ne);
+  }
+}
+
+// dense admissible blocks (block order): off_dense after the near field and
+// the host record {block | converged << 31, offset}
+__global__ void k_classify_dense(const int *list, const int *cnt, AcaDev S,
+                                 const longlong2 *scan, const longlong2 *dsz, const int *adm_leaf,
+                                 long long nf_entries, LeafMeta M, longlong2 *info) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= *cnt) return;
+  const int q = list[p];
+  const long long off = scan[q].x - dsz[q].x;
+  M.off_d[adm_leaf[q]] = nf_entries + off;
+  const long long conv = S.status[q] == ST_CONVERGED ? 1 : 0;
+  info[p] = make_longlong2((long long)q | (conv << 31), off);
+}
+
+__global__ void k_gather_ll(const int *list, int n, const long long *src, long long *dst) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) dst[p] = src[list[p]];
+}
+
 struct SumLL2 {
   __device__ __forceinline__ longlong2 operator()(const longlong2 &a, const longlong2 &b) const {
     return make_longlong2(a.x + b.x, a.y + b.y);
@@ -297,10 +361,9 @@ struct hbem_hmat {
   size_t vbytes = 8;
   int nt = 1, ns = 1;
   bool p0 = false;  // both spaces P0: register-resident record kernels
-  // per leaf results (host)
-  std::vector<int32_t> kind, rank, flags;
-  std::vector<int64_t> off_u, off_v, off_dense;
-  std::vector<double> resid;
+  // per leaf results (device; near-field entries written once at setup,
+  // admissible ones by k_classify every execute)
+  LeafMeta meta{};
   // partition views (device)
   const int *rperm = nullptr, *cperm = nullptr;
   const int *tptr = nullptr, *tel = nullptr, *sptr = nullptr, *sel = nullptr;
@@ -327,7 +390,7 @@ struct hbem_hmat {
   VPool vpool;  // ACA factor pool
   Geo64 *g64p = nullptr;  // device copy of the context's float64 geometry view
   // pinned mailbox for the per-phase host reads
-  struct Mail { Need tot; int n; int pad; } *mail = nullptr;
+  struct Mail { Need tot; int n; int pad; int cls_cnt[2]; ClsStat cls; long long adm_dense; } *mail = nullptr;
   // near-field leaves
   int nd = 0;
   std::vector<int> den_leaf;
@@ -340,7 +403,12 @@ struct hbem_hmat {
   void *dense_adm = nullptr;
   size_t dense_adm_cap = 0;
   long long dense_entries = 0, u_entries = 0, v_entries = 0;
-  std::vector<int> lowrank_slots;
+  // block lists of the last execute (device, block order)
+  int *d_adm_leaf = nullptr, *lr_list = nullptr, *dn_list = nullptr, *cls_cnt = nullptr;
+  unsigned char *cls_flag = nullptr;
+  ClsStat *cls_stat = nullptr;
+  longlong2 *dn_info = nullptr;
+  int n_lowrank = 0;
   // matvec: admissible blocks stored densely (host lists, uploaded lazily)
   std::vector<int> ad_r0, ad_c0, ad_h, ad_w;
   std::vector<long long> ad_off, ad_rowbase;
@@ -348,9 +416,8 @@ struct hbem_hmat {
   const long long *nf_rowbase = nullptr;
   bool mv_dirty = true;
   void *mv_buf = nullptr;  // x, y, xt, yt
-  int *mv_lr = nullptr, *mv_ad = nullptr;
+  int *mv_ad = nullptr;
   long long *mv_ad_l = nullptr;
-  std::vector<int64_t> lr_uoff, lr_voff;
   // streamed payloads: per-wave packing of converged low-rank blocks into
   // device U / V arenas (growable), optional D2H into caller host arenas
   VPool uarena, varena;
@@ -389,7 +456,6 @@ struct hbem_hmat {
     cudaFree(partC);
     cudaFree(rsc);
     cudaFree(mv_buf);
-    cudaFree(mv_lr);
     cudaFree(mv_ad);
     cudaFree(mv_ad_l);
     if (mail) cudaFreeHost(mail);
@@ -589,13 +655,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   }
   const int64_t L = d->n_leaves;
   H->n_leaves = L;
-  H->kind.assign(L, 0);
-  H->rank.assign(L, 0);
-  H->flags.assign(L, 0);
-  H->off_u.assign(L, -1);
-  H->off_v.assign(L, -1);
-  H->off_dense.assign(L, -1);
-  H->resid.assign(L, 0.0);
+  std::vector<long long> off_dense0(L, -1);  // near-field leaves: fixed offsets
   for (int64_t q = 0; q < L; ++q)
     (d->leaves[3 * q + 2] ? H->adm_leaf : H->den_leaf).push_back((int)q);
   auto rng = [&](const int64_t *nodes, int64_t n) {
@@ -754,7 +814,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
     auto [c0, w] = rng(d->col_nodes, d->leaves[3 * lf + 1]);
     dr0[q] = r0; dh[q] = h; dc0[q] = c0; dw[q] = w;
     doff[q] = tot;
-    H->off_dense[lf] = tot;
+    off_dense0[lf] = tot;
     tot += (long long)h * w;
   }
   H->nf_entries = tot;
@@ -821,6 +881,26 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
       HB_CHECK(upload(H, &p, tslot)); D.tile_slot = p;
       HB_CHECK(upload(H, &p, tstart)); D.tile_start = p;
     }
+  }
+  {
+    // per-leaf metadata on the device: near-field leaves are dense, rank 0
+    LeafMeta &M = H->meta;
+    HB_CHECK(dalloc(H, &M.kind, (size_t)std::max<int64_t>(3 * L, 1)));
+    M.rank = M.kind + L;
+    M.flags = M.kind + 2 * L;
+    HB_CHECK(dalloc(H, &M.off_u, (size_t)std::max<int64_t>(3 * L, 1)));
+    M.off_v = M.off_u + L;
+    M.off_d = M.off_u + 2 * L;
+    HB_CUDA(cudaMemset(M.kind, 0, (size_t)3 * L * 4));
+    HB_CUDA(cudaMemset(M.off_u, 0xff, (size_t)2 * L * 8));
+    HB_CUDA(cudaMemcpy(M.off_d, off_dense0.data(), (size_t)L * 8, cudaMemcpyHostToDevice));
+    HB_CHECK(upload(H, &H->d_adm_leaf, H->adm_leaf));
+    HB_CHECK(dalloc(H, &H->lr_list, std::max(na, 1)));
+    HB_CHECK(dalloc(H, &H->dn_list, std::max(na, 1)));
+    HB_CHECK(dalloc(H, &H->cls_cnt, 2));
+    HB_CHECK(dalloc(H, &H->cls_flag, (size_t)2 * std::max(na, 1)));
+    HB_CHECK(dalloc(H, &H->cls_stat, 1));
+    HB_CHECK(dalloc(H, &H->dn_info, std::max(na, 1)));
   }
   const size_t vb = H->vbytes;
   HB_CUDA(cudaMalloc(&H->dense_nf, std::max<size_t>((size_t)tot * vb, vb)));
@@ -1150,66 +1230,75 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   H->packed = H->streaming();
   const auto t_aca = clk::now();
   // ---- classify admissible blocks (lowrank_leaf, hmatrix.py:721-735) -------------
-  std::vector<int> st_h(na), rk_h(na), ex_h(na);
-  std::vector<double> rs_h(na);
-  std::vector<long long> bu_h(na), bv_h(na);
-  if (na > 0) {
-    HB_CUDA(cudaMemcpy(bu_h.data(), H->blk_uoff, (size_t)na * 8, cudaMemcpyDeviceToHost));
-    HB_CUDA(cudaMemcpy(bv_h.data(), H->blk_voff, (size_t)na * 8, cudaMemcpyDeviceToHost));
-    HB_CUDA(cudaMemcpy(st_h.data(), S.status, na * 4, cudaMemcpyDeviceToHost));
-    HB_CUDA(cudaMemcpy(rk_h.data(), S.rank, na * 4, cudaMemcpyDeviceToHost));
-    HB_CUDA(cudaMemcpy(ex_h.data(), S.exhausted, na * 4, cudaMemcpyDeviceToHost));
-    HB_CUDA(cudaMemcpy(rs_h.data(), S.resid, na * 8, cudaMemcpyDeviceToHost));
-  }
-  H->lowrank_slots.clear();
-  H->lr_uoff.clear();
-  H->lr_voff.clear();
-  H->u_entries = H->v_entries = 0;
+  // on the device: per-leaf metadata in place, block-ordered low-rank and
+  // dense lists, dense offsets by a scan; the host reads the counters and the
+  // (short) dense list only
   std::vector<int> expand_slots, fb_r0, fb_c0, fb_h, fb_w;
   std::vector<long long> expand_off, fb_off;
+  std::vector<int> fb_q;
   long long adm_dense = 0;
-  for (int q = 0; q < na; ++q) {
-    const int lf = H->adm_leaf[q];
-    const int s = st_h[q];
-    const int h = H->ah[q], w = H->aw[q];
-    if (s == ST_OVERFLOW)
+  H->n_lowrank = 0;
+  if (na > 0) {
+    const unsigned g = (unsigned)((na + 255) / 256);
+    HB_CUDA(cudaMemsetAsync(H->cls_stat, 0, 16, st));
+    HB_CUDA(cudaMemsetAsync(&H->cls_stat->overflow_q, 0x7f, 4, st));
+    unsigned char *flr = H->cls_flag, *fdn = H->cls_flag + na;
+    k_classify<<<g, 256, 0, st>>>(S, na, H->d_adm_leaf, H->blk_uoff, H->blk_voff, H->meta,
+                                  H->emit_need, flr, fdn, H->cls_stat);
+    size_t tb = H->emit_tmp_bytes;
+    HB_CUDA(cub::DeviceScan::InclusiveScan(H->emit_tmp, tb, H->emit_need, H->emit_scan, SumLL2(),
+                                           na, st));
+    tb = H->emit_tmp_bytes;
+    HB_CUDA(cub::DeviceSelect::Flagged(H->emit_tmp, tb, cub::CountingInputIterator<int>(0), flr,
+                                       H->lr_list, H->cls_cnt, na, st));
+    tb = H->emit_tmp_bytes;
+    HB_CUDA(cub::DeviceSelect::Flagged(H->emit_tmp, tb, cub::CountingInputIterator<int>(0), fdn,
+                                       H->dn_list, H->cls_cnt + 1, na, st));
+    k_classify_dense<<<g, 256, 0, st>>>(H->dn_list, H->cls_cnt + 1, S, H->emit_scan,
+                                        H->emit_need, H->d_adm_leaf, H->nf_entries, H->meta,
+                                        H->dn_info);
+    HB_CUDA(cudaGetLastError());
+    launches += 6;
+    auto *ml = H->mail;
+    HB_CUDA(cudaMemcpyAsync(ml->cls_cnt, H->cls_cnt, 8, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaMemcpyAsync(&ml->cls, H->cls_stat, sizeof(ClsStat), cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaMemcpyAsync(&ml->adm_dense, &H->emit_scan[na - 1].x, 8, cudaMemcpyDeviceToHost,
+                            st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    if (ml->cls.overflow_q < na) {
+      const int q = ml->cls.overflow_q;
       return set_error(HBEM_ERR_CAPACITY,
                        "ACA rank capacity %d exceeded for block rows [%d, %d) x cols [%d, %d); "
                        "raise rank_capacity",
-                       S.tmax, H->ar0[q], H->ar0[q] + h, H->ac0[q], H->ac0[q] + w);
-    H->rank[lf] = rk_h[q];
-    H->resid[lf] = rs_h[q];
-    H->flags[lf] = (s == ST_CONVERGED ? 1 : 0) | (ex_h[q] ? 2 : 0);
-    H->kind[lf] = 0;
-    H->off_u[lf] = H->off_v[lf] = -1;
-    const long long hw = (long long)h * w;
-    if (ex_h[q]) ST.aca_exhausted++;
-    if (s == ST_CONVERGED) {
-      ST.aca_converged++;
-      if ((long long)rk_h[q] * (h + w) < hw) {
-        // packed by emit_converged in the wave it converged
-        H->kind[lf] = 1;
-        H->lowrank_slots.push_back(q);
-        H->off_u[lf] = bu_h[q];
-        H->off_v[lf] = bv_h[q];
-        H->lr_uoff.push_back(bu_h[q]);
-        H->lr_voff.push_back(bv_h[q]);
-        ST.lowrank_leaves++;
-        continue;
-      }
-      expand_slots.push_back(q);
-      expand_off.push_back(adm_dense);
-    } else {  // ST_FALLBACK: rank cap without convergence -> exact rows
-      ST.aca_fallback_dense++;
-      fb_r0.push_back(H->ar0[q]); fb_c0.push_back(H->ac0[q]);
-      fb_h.push_back(h); fb_w.push_back(w);
-      fb_off.push_back(adm_dense);
+                       S.tmax, H->ar0[q], H->ar0[q] + H->ah[q], H->ac0[q], H->ac0[q] + H->aw[q]);
     }
-    H->off_dense[lf] = H->nf_entries + adm_dense;
-    adm_dense += hw;
+    H->n_lowrank = ml->cls_cnt[0];
+    const int n_dn = ml->cls_cnt[1];
+    adm_dense = ml->adm_dense;
+    ST.aca_converged = (int64_t)ml->cls.converged;
+    ST.aca_exhausted = (int64_t)ml->cls.exhausted;
+    ST.lowrank_leaves = H->n_lowrank;
+    std::vector<longlong2> info(n_dn);
+    if (n_dn > 0)
+      HB_CUDA(cudaMemcpy(info.data(), H->dn_info, (size_t)n_dn * sizeof(longlong2),
+                         cudaMemcpyDeviceToHost));
+    for (const longlong2 &r : info) {
+      const int q = (int)(r.x & 0x7fffffffll);
+      if (r.x >> 31) {  // converged, no compression: expanded from the factors
+        expand_slots.push_back(q);
+        expand_off.push_back(r.y);
+      } else {          // ST_FALLBACK: rank cap without convergence -> exact rows
+        ST.aca_fallback_dense++;
+        fb_q.push_back(q);
+        fb_r0.push_back(H->ar0[q]); fb_c0.push_back(H->ac0[q]);
+        fb_h.push_back(H->ah[q]); fb_w.push_back(H->aw[q]);
+        fb_off.push_back(r.y);
+      }
+    }
   }
   H->u_entries = H->u_top;
   H->v_entries = H->v_top;
+  const auto t_cls = clk::now();
   ST.dense_leaves = H->nd + (int64_t)expand_slots.size() + (int64_t)fb_r0.size();
   H->ad_r0.clear(); H->ad_c0.clear(); H->ad_h.clear(); H->ad_w.clear();
   H->ad_off.clear(); H->ad_rowbase.clear();
@@ -1222,9 +1311,7 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
       rows += H->ah[q];
     };
     for (size_t z = 0; z < expand_slots.size(); ++z) add(expand_slots[z], expand_off[z]);
-    size_t fz = 0;
-    for (int q = 0; q < na && fz < fb_off.size(); ++q)
-      if (st_h[q] != ST_CONVERGED) add(q, fb_off[fz++]);
+    for (size_t z = 0; z < fb_q.size(); ++z) add(fb_q[z], fb_off[z]);
   }
   H->mv_dirty = true;
   H->dense_entries = H->nf_entries + adm_dense;
@@ -1317,6 +1404,7 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   }
   HB_CUDA(cudaStreamSynchronize(H->cp));
   HB_CUDA(cudaStreamSynchronize(H->cpd));
+  const auto t_pre_wait = clk::now();
   HB_CUDA(cudaStreamWaitEvent(st, H->side_done, 0));
   unsigned long long nf_sing = 0, nf_stat[2] = {0, 0}, aca_stat[2] = {0, 0};
   HB_CUDA(cudaMemcpyAsync(&nf_sing, H->D.sing_count, 8, cudaMemcpyDeviceToHost, st));
@@ -1324,6 +1412,10 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   HB_CUDA(cudaMemcpyAsync(aca_stat, S.stat, 16, cudaMemcpyDeviceToHost, st));
   HB_CUDA(cudaStreamSynchronize(st));
   const auto t_end = clk::now();
+  if (std::getenv("HBEM_TRACE"))
+    std::fprintf(stderr, "[hbem execute] waves %.4f classify %.4f expand/fallback %.4f "
+                 "near-field wait + stats %.4f s\n", secs(t0, t_aca), secs(t_aca, t_cls),
+                 secs(t_cls, t_pre_wait), secs(t_pre_wait, t_end));
   {
     float ms = 0.f;
     HB_CUDA(cudaEventElapsedTime(&ms, H->ev[2], H->ev[3]));
@@ -1428,12 +1520,16 @@ int hbem_hmat_stats_get(const hbem_hmat *h, hbem_hmat_stats *s) {
 int hbem_hmat_leaf_meta(const hbem_hmat *h, int32_t *kind, int32_t *rank, int32_t *flags,
                         int64_t *off_u, int64_t *off_v, int64_t *off_dense) {
   if (!h) return set_error(HBEM_ERR_ARG, "null hmat");
-  if (kind) std::copy(h->kind.begin(), h->kind.end(), kind);
-  if (rank) std::copy(h->rank.begin(), h->rank.end(), rank);
-  if (flags) std::copy(h->flags.begin(), h->flags.end(), flags);
-  if (off_u) std::copy(h->off_u.begin(), h->off_u.end(), off_u);
-  if (off_v) std::copy(h->off_v.begin(), h->off_v.end(), off_v);
-  if (off_dense) std::copy(h->off_dense.begin(), h->off_dense.end(), off_dense);
+  clear_error();
+  HB_CUDA(cudaSetDevice(h->device));
+  const size_t L = (size_t)h->n_leaves;
+  const LeafMeta &M = h->meta;
+  if (kind) HB_CUDA(cudaMemcpy(kind, M.kind, L * 4, cudaMemcpyDeviceToHost));
+  if (rank) HB_CUDA(cudaMemcpy(rank, M.rank, L * 4, cudaMemcpyDeviceToHost));
+  if (flags) HB_CUDA(cudaMemcpy(flags, M.flags, L * 4, cudaMemcpyDeviceToHost));
+  if (off_u) HB_CUDA(cudaMemcpy(off_u, M.off_u, L * 8, cudaMemcpyDeviceToHost));
+  if (off_v) HB_CUDA(cudaMemcpy(off_v, M.off_v, L * 8, cudaMemcpyDeviceToHost));
+  if (off_dense) HB_CUDA(cudaMemcpy(off_dense, M.off_d, L * 8, cudaMemcpyDeviceToHost));
   return HBEM_OK;
 }
 
@@ -1477,19 +1573,12 @@ int hbem_hmat_copy_arenas(const hbem_hmat *hc, void *u, void *v, void *dense) {
     if (e != cudaSuccess) return fail(e);
   }
   // low-rank factors: packed per wave when streaming, else packed here
-  if (!h->packed && !h->lowrank_slots.empty()) {
-    const size_t n = h->lowrank_slots.size();
-    int *d_slots = nullptr;
-    long long *d_uo = nullptr, *d_vo = nullptr;
-    e = cudaMalloc(&d_slots, n * 4);
-    if (e == cudaSuccess) { tmp.push_back(d_slots); e = cudaMalloc(&d_uo, n * 8); }
-    if (e == cudaSuccess) { tmp.push_back(d_uo); e = cudaMalloc(&d_vo, n * 8); }
-    if (e == cudaSuccess) tmp.push_back(d_vo);
-    if (e == cudaSuccess)
-      e = cudaMemcpy(d_slots, h->lowrank_slots.data(), n * 4, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(d_uo, h->lr_uoff.data(), n * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(d_vo, h->lr_voff.data(), n * 8, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return fail(e);
+  if (!h->packed && h->n_lowrank > 0) {
+    const size_t n = (size_t)h->n_lowrank;
+    const int *d_slots = h->lr_list;
+    long long *d_uo = h->q_uoff, *d_vo = h->q_voff;  // free after the waves
+    k_gather_ll<<<(unsigned)((n + 255) / 256), 256, 0, sp[0]>>>(d_slots, (int)n, h->blk_uoff, d_uo);
+    k_gather_ll<<<(unsigned)((n + 255) / 256), 256, 0, sp[0]>>>(d_slots, (int)n, h->blk_voff, d_vo);
     if (h->uarena.grow((size_t)h->u_entries * vb) != HBEM_OK ||
         h->varena.grow((size_t)h->v_entries * vb) != HBEM_OK) {
       done();
@@ -1538,13 +1627,11 @@ int hbem_hmat_matvec(const hbem_hmat *hc, const void *x, void *y) {
   void *dx = buf, *dxt = buf + (size_t)nc * vb, *dy = buf + (size_t)2 * nc * vb,
        *dyt = buf + (size_t)(2 * nc + nr) * vb;
   if (h->mv_dirty) {
-    cudaFree(h->mv_lr); cudaFree(h->mv_ad); cudaFree(h->mv_ad_l);
-    h->mv_lr = nullptr; h->mv_ad = nullptr; h->mv_ad_l = nullptr;
-    const size_t nl = h->lowrank_slots.size(), na = h->ad_r0.size();
-    HB_CUDA(cudaMalloc(&h->mv_lr, std::max<size_t>(nl, 1) * 4));
+    cudaFree(h->mv_ad); cudaFree(h->mv_ad_l);
+    h->mv_ad = nullptr; h->mv_ad_l = nullptr;
+    const size_t na = h->ad_r0.size();
     HB_CUDA(cudaMalloc(&h->mv_ad, std::max<size_t>(na, 1) * 4 * 4));
     HB_CUDA(cudaMalloc(&h->mv_ad_l, std::max<size_t>(na, 1) * 8 * 2));
-    if (nl) HB_CUDA(cudaMemcpy(h->mv_lr, h->lowrank_slots.data(), nl * 4, cudaMemcpyHostToDevice));
     if (na) {
       HB_CUDA(cudaMemcpy(h->mv_ad, h->ad_r0.data(), na * 4, cudaMemcpyHostToDevice));
       HB_CUDA(cudaMemcpy(h->mv_ad + na, h->ad_c0.data(), na * 4, cudaMemcpyHostToDevice));
@@ -1569,8 +1656,8 @@ int hbem_hmat_matvec(const hbem_hmat *hc, const void *x, void *y) {
   M.dense[1] = MatvecArgs::Dense{na, h->mv_ad, h->mv_ad + na, h->mv_ad + 2 * na,
                                  h->mv_ad + 3 * na, h->mv_ad_l, h->mv_ad_l + na, ad_rows,
                                  h->dense_adm};
-  M.n_lowrank = (int)h->lowrank_slots.size();
-  M.lowrank = h->mv_lr;
+  M.n_lowrank = h->n_lowrank;
+  M.lowrank = h->lr_list;
   HB_CUDA(cudaMemcpy(dx, x, (size_t)nc * vb, cudaMemcpyHostToDevice));
   const hbem_ctx *ctx = h->ctx;
   int rc;
