@@ -28,6 +28,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <mutex>
+#include <initializer_list>
+#include <tuple>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -143,6 +146,53 @@ __global__ void k_pack_factors(const int *slots, int n, AcaDev S, const long lon
   }
 }
 
+// streamed emission straight into the caller's page-locked host arenas: SM
+// stores over PCIe (posted writes; a few CTAs saturate the link), a warp per
+// block, grid-stride; no device staging arena and no copy engine. Same
+// values as k_pack_factors bit for bit.
+template <typename Tr, bool Cc, typename V = typename Num<Tr, Cc>::V>
+__global__ void __launch_bounds__(256) k_pack_host(const int *slots, int n, AcaDev S,
+                                                   const long long *uoff, const long long *voff,
+                                                   V *u, V *v) {
+  using N = Num<Tr, Cc>;
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const V *pool = static_cast<const V *>(S.pool);
+  for (int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < n; q += nw) {
+    const int b = slots[q];
+    const int h = S.h[b], w = S.w[b], k = S.rank[b];
+    V *ub = u + uoff[q], *vb = v + voff[q];
+    const long long *terms = S.terms + (long long)b * S.tmax;
+    for (int l0 = 0; l0 < k; l0 += 32) {
+      // term offsets fetched lane-parallel, values loaded ahead of the
+      // (posted) PCIe stores: several independent loads in flight per lane
+      const long long my = l0 + lane < k ? terms[l0 + lane] : 0;
+      const int nl = min(32, k - l0);
+      for (int j = 0; j < nl; ++j) {
+        const V *t = pool + __shfl_sync(0xffffffffu, my, j);
+        const long long l = l0 + j;
+        const V p = t[h + w];
+        V ur[4], vr[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = lane + 32 * i, c = lane + 32 * i;
+          if (r < h) ur[i] = t[r];
+          if (c < w) vr[i] = t[h + c];
+        }
+        const V inv = N::div(N::mk(Tr(1), Tr(0)), p);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = lane + 32 * i, c = lane + 32 * i;
+          if (r < h) ub[l * h + r] = ur[i];
+          if (c < w) vb[l * w + c] = N::fma_acc(N::zero(), vr[i], inv);
+        }
+        for (int r = lane + 128; r < h; r += 32) ub[l * h + r] = t[r];
+        for (int c = lane + 128; c < w; c += 32) vb[l * w + c] = N::fma_acc(N::zero(), t[h + c], inv);
+      }
+    }
+  }
+}
+
 // per-wave emission of converged low-rank blocks (lowrank_leaf rule,
 // hmatrix.py:721-729): flags in block order, not yet emitted
 __global__ void k_emit_flags(AcaDev S, int na, unsigned char *emitted, unsigned char *flag) {
@@ -178,6 +228,21 @@ __global__ void k_emit_offsets(const int *list, int n, const longlong2 *scan,
   blk_voff[b] = vo;
   q_uoff[p] = uo;
   q_voff[p] = vo;
+}
+
+// small device -> host reads (phase totals, counters) by a one-warp kernel
+// storing into the mapped page-locked mailbox: a cudaMemcpyAsync D2H would
+// queue on the copy engine behind the multi-GB payload copies and stall the
+// wave loop on them
+struct MailCopy {
+  const unsigned *src[3];
+  unsigned *dst[3];
+  int words[3];
+};
+
+__global__ void k_mail(MailCopy m) {
+  for (int r = 0; r < 3; ++r)
+    for (int i = threadIdx.x; i < m.words[r]; i += blockDim.x) m.dst[r][i] = m.src[r][i];
 }
 
 // classification of every admissible block after the waves (lowrank_leaf /
@@ -290,9 +355,11 @@ struct VmmApi {
 };
 static VmmApi g_vmm;
 
+
 struct VPool {
   CUdeviceptr base = 0;
   size_t reserved = 0, mapped = 0, step = 0;
+  double grow_s = 0.0;  // host time spent mapping (trace)
   std::vector<CUmemGenericAllocationHandle> handles;
   std::vector<size_t> sizes;
   CUmemAllocationProp prop{};
@@ -317,6 +384,13 @@ struct VPool {
   }
   // map until at least `bytes` are backed
   int grow(size_t bytes) {
+    if (mapped >= bytes) return HBEM_OK;
+    const auto t0 = std::chrono::steady_clock::now();
+    struct Acc {
+      double &s;
+      std::chrono::steady_clock::time_point t;
+      ~Acc() { s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count(); }
+    } acc_{grow_s, t0};
     while (mapped < bytes) {
       if (mapped + step > reserved)
         return set_error(HBEM_ERR_CAPACITY, "ACA factor pool exhausted (%zu bytes reserved)",
@@ -391,6 +465,23 @@ struct hbem_hmat {
   Geo64 *g64p = nullptr;  // device copy of the context's float64 geometry view
   // pinned mailbox for the per-phase host reads
   struct Mail { Need tot; int n; int pad; int cls_cnt[2]; ClsStat cls; long long adm_dense; } *mail = nullptr;
+  char *mail_dev = nullptr;  // device view of the mailbox
+  // D2H of up to three small device ranges into mailbox fields (k_mail)
+  int read_mail(cudaStream_t st, std::initializer_list<std::tuple<void *, const void *, size_t>> r) {
+    MailCopy m{};
+    int i = 0;
+    for (const auto &[dst, src, bytes] : r) {
+      m.dst[i] = reinterpret_cast<unsigned *>(mail_dev + (static_cast<char *>(dst) -
+                                                          reinterpret_cast<char *>(mail)));
+      m.src[i] = static_cast<const unsigned *>(src);
+      m.words[i] = (int)(bytes / 4);
+      ++i;
+    }
+    k_mail<<<1, 32, 0, st>>>(m);
+    HB_CUDA(cudaGetLastError());
+    HB_CUDA(cudaStreamSynchronize(st));
+    return HBEM_OK;
+  }
   // near-field leaves
   int nd = 0;
   std::vector<int> den_leaf;
@@ -431,6 +522,7 @@ struct hbem_hmat {
   bool packed = false;  // U / V arenas hold the current factors
   bool streaming() const { return out_u || out_v || out_dense; }
   void *out_u = nullptr, *out_v = nullptr, *out_dense = nullptr;
+  void *zc_u = nullptr, *zc_v = nullptr;  // device views of out_u / out_v (zero-copy)
   long long out_u_cap = 0, out_v_cap = 0, out_dense_cap = 0;
   cudaStream_t cp = nullptr;    // factor packing + D2H, middle priority
   cudaStream_t cpd = nullptr;   // dense-arena D2H (waits for the near field)
@@ -519,10 +611,11 @@ template <typename X> int upload(hbem_hmat *H, X **p, const std::vector<X> &v) {
   return HBEM_OK;
 }
 
-// grow-only device scratch (stream must be idle)
-int ensure(double **p, size_t *cap, size_t need) {
+// grow-only device scratch; the old buffer is retired until the next execute
+// (cudaFree would synchronise the device, stalling the payload copies)
+int ensure(std::vector<void *> &retire, double **p, size_t *cap, size_t need) {
   if (need <= *cap) return HBEM_OK;
-  cudaFree(*p);
+  if (*p) retire.push_back(*p);
   *p = nullptr;
   *cap = 0;
   const size_t n = std::max(need + need / 4, (size_t)1 << 16);
@@ -801,6 +894,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   H->cub_bytes = aca_cub_bytes(na);
   HB_CHECK(dalloc(H, (char **)&H->cub_tmp, H->cub_bytes));
   HB_CUDA(cudaMallocHost(&H->mail, sizeof(hbem_hmat::Mail)));
+  HB_CUDA(cudaHostGetDevicePointer((void **)&H->mail_dev, H->mail, 0));
   tr.mark("admissible blocks");
   // ---- near-field leaves --------------------------------------------------------
   const int nd = (int)H->den_leaf.size();
@@ -965,6 +1059,23 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   H->out_u_cap = d->out_u_cap;
   H->out_v_cap = d->out_v_cap;
   H->out_dense_cap = d->out_dense_cap;
+  {
+    // page-locked U / V arenas are device-addressable: with HBEM_ZEROCOPY=1
+    // the emission kernel writes them directly over PCIe (no device staging
+    // arena, 56 GB less HBM at C5); the default stages the packed factors in
+    // HBM and moves them with the copy engine, which sustains the PCIe rate
+    // without taking SM slots from the ACA waves
+    const char *zc_env = std::getenv("HBEM_ZEROCOPY");
+    if (H->out_u && H->out_v && zc_env && zc_env[0] == '1') {
+      void *pu = nullptr, *pv = nullptr;
+      if (cudaHostGetDevicePointer(&pu, H->out_u, 0) == cudaSuccess &&
+          cudaHostGetDevicePointer(&pv, H->out_v, 0) == cudaSuccess) {
+        H->zc_u = pu;
+        H->zc_v = pv;
+      }
+      cudaGetLastError();
+    }
+  }
   HB_CUDA(cudaEventCreateWithFlags(&H->side_done, cudaEventDisableTiming));
   for (auto &e : H->ev) HB_CUDA(cudaEventCreate(&e));
   for (auto &pr : H->iev)
@@ -990,10 +1101,8 @@ int run_phase(hbem_hmat *H, const Prob<T> &P, int col, long long &pool_top, int 
   S.list = col ? H->listC : H->listA;
   S.nlist = H->d_cnt;
   HB_CHECK((aca_select<T, C>(P, S, A, st)));
-  HB_CUDA(cudaMemcpyAsync(&H->mail->tot, S.scan + (H->na - 1), sizeof(Need),
-                          cudaMemcpyDeviceToHost, st));
-  HB_CUDA(cudaMemcpyAsync(&H->mail->n, H->d_cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
-  HB_CUDA(cudaStreamSynchronize(st));
+  HB_CHECK(H->read_mail(st, {{&H->mail->tot, S.scan + (H->na - 1), sizeof(Need)},
+                             {&H->mail->n, H->d_cnt, sizeof(int)}}));
   const Need tot = H->mail->tot;
   const int n = H->mail->n;
   *n_out = n;
@@ -1011,11 +1120,11 @@ int run_phase(hbem_hmat *H, const Prob<T> &P, int col, long long &pool_top, int 
     return set_error(HBEM_ERR_CAPACITY, "ACA item table overflow (%lld > %lld)",
                      (long long)tot.items, (long long)H->items_cap);
   if (col) {
-    HB_CHECK(ensure(&H->partC, &H->partC_cap, (size_t)tot.part));
+    HB_CHECK(ensure(H->exec_allocs, &H->partC, &H->partC_cap, (size_t)tot.part));
     S.part = H->partC;
     S.rpart = H->partA;
   } else {
-    HB_CHECK(ensure(&H->partA, &H->partA_cap, (size_t)tot.part));
+    HB_CHECK(ensure(H->exec_allocs, &H->partA, &H->partA_cap, (size_t)tot.part));
     S.part = H->partA;
   }
   A.int_beg = H->iev[col][0];
@@ -1028,7 +1137,7 @@ int run_phase(hbem_hmat *H, const Prob<T> &P, int col, long long &pool_top, int 
                        (long long)tot.eitems, (long long)H->eitems_cap);
     const size_t need = (size_t)std::max<long long>(tot.rsc, 1) * H->vbytes;
     if (need > H->rsc_cap) {
-      cudaFree(H->rsc);
+      if (H->rsc) H->exec_allocs.push_back(H->rsc);
       H->rsc = nullptr;
       const size_t cap = need + need / 4;
       cudaError_t e = cudaMalloc(&H->rsc, cap);
@@ -1061,15 +1170,14 @@ template <typename T, bool C> int emit_converged(hbem_hmat *H, cudaStream_t st, 
   tb = H->emit_tmp_bytes;
   HB_CUDA(cub::DeviceScan::InclusiveScan(H->emit_tmp, tb, H->emit_need, H->emit_scan, SumLL2(),
                                          na, st));
-  HB_CUDA(cudaMemcpyAsync(&H->mail->tot, H->emit_scan + (na - 1), sizeof(longlong2),
-                          cudaMemcpyDeviceToHost, st));
-  HB_CUDA(cudaMemcpyAsync(&H->mail->n, H->emit_cnt, sizeof(int), cudaMemcpyDeviceToHost, st));
-  HB_CUDA(cudaStreamSynchronize(st));
+  HB_CHECK(H->read_mail(st, {{&H->mail->tot, H->emit_scan + (na - 1), sizeof(longlong2)},
+                             {&H->mail->n, H->emit_cnt, sizeof(int)}}));
   const int n = H->mail->n;
   const longlong2 tot = *reinterpret_cast<const longlong2 *>(&H->mail->tot);
   if (n == 0) return HBEM_OK;
   const size_t vb = sizeof(V);
-  if (pack) {
+  const bool zc = pack && H->zc_u && H->zc_v;
+  if (pack && !zc) {
     HB_CHECK(H->uarena.grow((size_t)(H->u_top + tot.x) * vb));
     HB_CHECK(H->varena.grow((size_t)(H->v_top + tot.y) * vb));
   }
@@ -1098,6 +1206,14 @@ template <typename T, bool C> int emit_converged(hbem_hmat *H, cudaStream_t st, 
   HB_CUDA(cudaMemcpyAsync(lst, H->emit_list, (size_t)n * 4, cudaMemcpyDeviceToDevice, H->cp));
   HB_CUDA(cudaMemcpyAsync(uo, H->q_uoff, (size_t)n * 8, cudaMemcpyDeviceToDevice, H->cp));
   HB_CUDA(cudaMemcpyAsync(vo, H->q_voff, (size_t)n * 8, cudaMemcpyDeviceToDevice, H->cp));
+  if (zc) {
+    k_pack_host<T, C><<<std::min((n + 7) / 8, 64), 256, 0, H->cp>>>(
+        lst, n, S, uo, vo, static_cast<V *>(H->zc_u), static_cast<V *>(H->zc_v));
+    HB_CUDA(cudaGetLastError());
+    H->u_top += tot.x;
+    H->v_top += tot.y;
+    return HBEM_OK;
+  }
   V *ua = reinterpret_cast<V *>(H->uarena.base), *va = reinterpret_cast<V *>(H->varena.base);
   k_pack_factors<T, C><<<n, 128, 0, H->cp>>>(lst, n, S, uo, vo, 0, 0, ua, va);
   HB_CUDA(cudaGetLastError());
@@ -1193,6 +1309,16 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   HB_CUDA(cudaMemsetAsync(S.stat, 0, 32, st));
   int waves = 0;
   long long pool_top = 0;
+  // HBEM_TRACE: per-wave timeline (host clock, copy-stream completion)
+  const bool wtrace = std::getenv("HBEM_TRACE") != nullptr;
+  cudaEvent_t wt0 = nullptr;
+  std::vector<cudaEvent_t> wcp;
+  std::vector<double> whost;
+  std::vector<long long> wbytes;
+  if (wtrace) {
+    HB_CUDA(cudaEventCreate(&wt0));
+    HB_CUDA(cudaEventRecord(wt0, st));
+  }
   if (na > 0) {
     HB_CHECK((aca_init<T, C>(P, S, na, st)));
     ++launches;
@@ -1202,7 +1328,16 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
       HB_CHECK((run_phase<T, C>(H, P, 0, pool_top, waves, &nA, st)));
       if (nA == 0) break;
       HB_CHECK((run_phase<T, C>(H, P, 1, pool_top, waves, &nC, st)));
+      const long long top0 = H->u_top + H->v_top;
       if (H->streaming()) HB_CHECK((emit_converged<T, C>(H, st)));
+      if (wtrace) {
+        cudaEvent_t e;
+        HB_CUDA(cudaEventCreate(&e));
+        HB_CUDA(cudaEventRecord(e, H->streaming() ? H->cp : st));
+        wcp.push_back(e);
+        whost.push_back(secs(t0, clk::now()));
+        wbytes.push_back((H->u_top + H->v_top - top0) * (long long)sizeof(V));
+      }
       launches += (nC > 0 ? 10 : 7) + (H->streaming() ? 4 : 0);
       HB_CUDA(cudaEventRecord(H->ev[1], st));
       HB_CUDA(cudaEventSynchronize(H->ev[1]));
@@ -1227,7 +1362,8 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
     // hbem_hmat_copy_arenas (the device-resident H-matrix is the pool)
     HB_CHECK((emit_converged<T, C>(H, st, /*pack=*/false)));
   }
-  H->packed = H->streaming();
+  // zero-copy emission leaves the device U / V arenas unpacked
+  H->packed = H->streaming() && !(H->zc_u && H->zc_v);
   const auto t_aca = clk::now();
   // ---- classify admissible blocks (lowrank_leaf, hmatrix.py:721-735) -------------
   // on the device: per-leaf metadata in place, block-ordered low-rank and
@@ -1260,11 +1396,9 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
     HB_CUDA(cudaGetLastError());
     launches += 6;
     auto *ml = H->mail;
-    HB_CUDA(cudaMemcpyAsync(ml->cls_cnt, H->cls_cnt, 8, cudaMemcpyDeviceToHost, st));
-    HB_CUDA(cudaMemcpyAsync(&ml->cls, H->cls_stat, sizeof(ClsStat), cudaMemcpyDeviceToHost, st));
-    HB_CUDA(cudaMemcpyAsync(&ml->adm_dense, &H->emit_scan[na - 1].x, 8, cudaMemcpyDeviceToHost,
-                            st));
-    HB_CUDA(cudaStreamSynchronize(st));
+    HB_CHECK(H->read_mail(st, {{ml->cls_cnt, H->cls_cnt, 8},
+                               {&ml->cls, H->cls_stat, sizeof(ClsStat)},
+                               {&ml->adm_dense, &H->emit_scan[na - 1].x, 8}}));
     if (ml->cls.overflow_q < na) {
       const int q = ml->cls.overflow_q;
       return set_error(HBEM_ERR_CAPACITY,
@@ -1317,7 +1451,7 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   H->dense_entries = H->nf_entries + adm_dense;
   const size_t vb = sizeof(V);
   if ((size_t)adm_dense * vb > H->dense_adm_cap) {
-    cudaFree(H->dense_adm);
+    if (H->dense_adm) H->exec_allocs.push_back(H->dense_adm);  // no device sync here
     H->dense_adm = nullptr;
     H->dense_adm_cap = (size_t)adm_dense * vb;
     HB_CUDA(cudaMalloc(&H->dense_adm, std::max(H->dense_adm_cap, vb)));
@@ -1412,10 +1546,23 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   HB_CUDA(cudaMemcpyAsync(aca_stat, S.stat, 16, cudaMemcpyDeviceToHost, st));
   HB_CUDA(cudaStreamSynchronize(st));
   const auto t_end = clk::now();
+  if (wtrace) {
+    for (size_t i = 0; i < wcp.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, wt0, wcp[i]);
+      std::fprintf(stderr, "[hbem wave %2zu] host %.4f s  copies done %.4f s  %.2f GB\n", i,
+                   whost[i], ms / 1e3, wbytes[i] / 1e9);
+      cudaEventDestroy(wcp[i]);
+    }
+    cudaEventDestroy(wt0);
+  }
   if (std::getenv("HBEM_TRACE"))
     std::fprintf(stderr, "[hbem execute] waves %.4f classify %.4f expand/fallback %.4f "
-                 "near-field wait + stats %.4f s\n", secs(t0, t_aca), secs(t_aca, t_cls),
-                 secs(t_cls, t_pre_wait), secs(t_pre_wait, t_end));
+                 "near-field wait + stats %.4f s; mapping pool %.3f u %.3f v %.3f s "
+                 "(%.1f / %.1f / %.1f GB)\n", secs(t0, t_aca), secs(t_aca, t_cls),
+                 secs(t_cls, t_pre_wait), secs(t_pre_wait, t_end), H->vpool.grow_s,
+                 H->uarena.grow_s, H->varena.grow_s, H->vpool.mapped / 1e9,
+                 H->uarena.mapped / 1e9, H->varena.mapped / 1e9);
   {
     float ms = 0.f;
     HB_CUDA(cudaEventElapsedTime(&ms, H->ev[2], H->ev[3]));

@@ -144,3 +144,53 @@ def test_hull_hmatrix_matches_reference():
     for x, yr in zip(g["x"], g["y"]):
         y = h.matvec(x)
         assert np.abs(y - yr).max() <= 1e-10 * np.abs(yr).max()
+
+
+@pytest.mark.parametrize("eq,k,zc", [("laplace", 0.0, "1"), ("laplace", 0.0, "0"),
+                                     ("helmholtz", 5.0, "1")])
+def test_streamed_payloads_equal_deferred_copy(monkeypatch, eq, k, zc):
+    """Payloads streamed during the assembly into page-locked host arenas
+    (zero-copy emission kernel, or the staged copy-engine path with
+    HBEM_ZEROCOPY=0) equal the deferred hbem_hmat_copy_arenas payloads bit for
+    bit, leaf by leaf (the streamed arenas are in convergence order), also
+    after a re-execute of the streamed handle and after a later on-demand
+    copy_arenas of it."""
+    from paper_1711_01897_b200.backend import init_gpu_device
+    from paper_1711_01897_b200.discretization import make_integration_context
+    from paper_1711_01897_b200.hmatrix import (AcaConfig, AssemblyConfig, _assemble_part,
+                                               pinned_empty)
+    monkeypatch.setenv("HBEM_ZEROCOPY", zc)
+    v, e, spec, sp, bt = problem(30, "p0", eq, "slp", k)
+    dev = init_gpu_device(make_integration_context(spec, sp, sp))
+    ids = np.arange(len(bt.leaf_array))
+    cfg, acfg = AcaConfig(epsilon=1e-4), AssemblyConfig()
+    ref = _assemble_part(dev, bt, ids, sp, sp, cfg, acfg)
+    s = ref.stats
+    dt = ref.arenas()[0].dtype
+    out = tuple(pinned_empty(s[n] + 17, dt) for n in ("u_entries", "v_entries", "dense_entries"))
+    part = _assemble_part(dev, bt, ids, sp, sp, cfg, acfg, out=out)
+
+    def same_payloads():
+        n_lr = 0
+        for q in range(len(ids)):
+            a, b = ref.payload(q), part.payload(q)
+            assert type(a) is type(b)
+            if hasattr(a, "u"):
+                n_lr += 1
+                assert np.array_equal(a.u, b.u) and np.array_equal(a.v, b.v), q
+            else:
+                assert np.array_equal(a.a, b.a), q
+        assert n_lr > 0
+
+    same_payloads()
+    for a in out:
+        a[:] = 0
+    part.execute()
+    same_payloads()
+    # on-demand copy of the same handle (device U / V packed here after a
+    # zero-copy run)
+    part._arenas = None
+    part._streamed = False
+    same_payloads()
+    part.close()
+    ref.close()
