@@ -174,14 +174,14 @@ class _DevicePart:
     def _refresh(self):
         L, handle = self.n_leaves, self.handle
         if getattr(self, "kind", None) is None:
-            # page-locked, allocated once: the per-leaf metadata is copied
-            # straight from the device arrays on every execute
-            self.kind = pinned_empty(L, np.int32)
-            self.rank = pinned_empty(L, np.int32)
-            self.flags = pinned_empty(L, np.int32)
-            self.off_u = pinned_empty(L, np.int64)
-            self.off_v = pinned_empty(L, np.int64)
-            self.off_d = pinned_empty(L, np.int64)
+            # allocated once, refilled from the device arrays on every execute
+            # (page-locking ~150 MB at C5 would cost more than it saves)
+            self.kind = np.empty(L, np.int32)
+            self.rank = np.empty(L, np.int32)
+            self.flags = np.empty(L, np.int32)
+            self.off_u = np.empty(L, np.int64)
+            self.off_v = np.empty(L, np.int64)
+            self.off_d = np.empty(L, np.int64)
         check(lib.hbem_hmat_leaf_meta(handle, _lib.ptr(self.kind, C.c_int32),
                                       _lib.ptr(self.rank, C.c_int32),
                                       _lib.ptr(self.flags, C.c_int32),
