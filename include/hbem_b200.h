@@ -219,6 +219,22 @@ int hbem_hmat_copy_arenas(const hbem_hmat *h, void *u, void *v, void *dense);
 int hbem_hmat_matvec(const hbem_hmat *h, const void *x, void *y);
 int hbem_hmat_destroy(hbem_hmat *h);
 
+/* Far-field potential of a surface density, evaluate_far_field
+   (scatter.py:362-408): out[i] = sum over elements e and rule points q of
+   K_dlp(points[i], y_eq) dens_eq with dens_eq = (sum_l phi[dofmap[e,l]]
+   table[l,q]) |J_e| w_q; K_dlp the Helmholtz (wavenumber > 0) or Laplace
+   (wavenumber == 0) double-layer kernel of kernel_planes (kernels.py:129-158).
+   points (n,3), vertices (nv,3), elements (m,3), rule_points (nq,2),
+   rule_weights (nq), table (local_dim,nq), dofmap (m,local_dim) row-major;
+   phi_im may be NULL (real density); r_min (n, nullable) receives each point's
+   distance to the nearest rule point (the near-field warning test). */
+int hbem_far_field(int32_t device, int64_t n_points, const double *points, int64_t n_vertices,
+                   const double *vertices, int64_t m, const int64_t *elements, int32_t nq,
+                   const double *rule_points, const double *rule_weights, int32_t local_dim,
+                   const double *table, const int64_t *dofmap, int64_t n_dofs,
+                   const double *phi_re, const double *phi_im, double wavenumber,
+                   double *out_re, double *out_im, double *r_min);
+
 /* pinned host buffers for fast D2H of the arenas */
 int hbem_host_alloc(int64_t bytes, void **out);
 int hbem_host_free(void *p);

@@ -804,3 +804,45 @@ def assemble_dense(P: Problem):
     for x, y in zip(a[touch], b[touch]):
         A[np.ix_(tdm[x], sdm[y])] += local_matrix(P, int(x), int(y))
     return A
+
+
+# ---------------------------------------------------------------------------
+# far-field potential                                  scatter.py:362-408
+# ---------------------------------------------------------------------------
+
+NEAR_FIELD_DIAMETERS = 3.0  # scatter.py:50
+
+
+def far_field(vertices, elements, family, dofmap, phi, points, k, quad_order=4, chunk=256):
+    """evaluate_far_field (scatter.py:362-408): dens = phi[dofmap] . table *
+    (|J| w) (374-376); per chunk of points diff = x - y_q, DLP kernel planes
+    with the element normal (385-388), sum over elements and rule points
+    (390).  Returns (u, n_near) with n_near the count of points closer than
+    3 element diameters to a rule point (379-384)."""
+    pts_r, w = regular_rule(quad_order)
+    v = vertices[elements]
+    e1 = v[:, 1] - v[:, 0]
+    e2 = v[:, 2] - v[:, 0]
+    cross = np.cross(e1, e2)
+    jac = np.linalg.norm(cross, axis=1)              # mesh.py:347-349
+    normals = cross / jac[:, None]
+    qpts = v[:, None, 0] + pts_r[None, :, 0, None] * e1[:, None] + pts_r[None, :, 1, None] * e2[:, None]
+    diam = np.stack([np.linalg.norm(e1, axis=1), np.linalg.norm(e2, axis=1),
+                     np.linalg.norm(v[:, 2] - v[:, 1], axis=1)]).max(axis=0)
+    table = basis_values(family, pts_r)
+    dens = np.einsum("ml,lq->mq", np.asarray(phi)[np.asarray(dofmap).reshape(len(elements), -1)],
+                     table)
+    dens = dens * (jac[:, None] * w[None, :])
+    d_near = NEAR_FIELD_DIAMETERS * float(diam.max())
+    out = np.empty(len(points), dtype=np.complex128)
+    n_near = 0
+    nrm = normals[None, :, None, :]
+    for lo in range(0, len(points), chunk):
+        hi = min(lo + chunk, len(points))
+        diff = points[lo:hi, None, None, :] - qpts[None, :, :, :]
+        r = np.sqrt(np.einsum("cmqi,cmqi->cmq", diff, diff))
+        n_near += int(np.count_nonzero(r.min(axis=(1, 2)) < d_near))
+        re, im = planes("dlp", k, diff, r, n_trial=nrm)
+        kern = re if im is None else re + 1j * im
+        out[lo:hi] = np.einsum("cmq,mq->c", kern, dens)
+    return out, n_near

@@ -137,6 +137,10 @@ SIGNATURES = [
     ("hbem_hmat_destroy", C.c_int, [C.c_void_p]),
     ("hbem_host_alloc", C.c_int, [C.c_int64, C.POINTER(C.c_void_p)]),
     ("hbem_host_free", C.c_int, [C.c_void_p]),
+    ("hbem_far_field", C.c_int, [C.c_int32, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("hbem_probe_fma", C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
 ]
 
