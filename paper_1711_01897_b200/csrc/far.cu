@@ -210,11 +210,17 @@ extern "C" int hbem_far_field(int32_t device, int64_t n_points, const double *po
     return e;
   };
   const long long mq = m * (long long)nq;
-  // element chunks so that (point tiles x chunks) fills the GPU ~4 CTAs per SM
+  // element chunks: (point tiles x chunks) just below four full waves of
+  // resident CTAs (a fraction of a wave left over would idle most SMs)
   const long long tiles = (n_points + kFarPts - 1) / kFarPts;
-  int sms = 148;
+  int sms = 148, per_sm = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  long long chunks = std::max<long long>(1, std::min<long long>((4ll * sms + tiles - 1) / tiles,
+  if (wavenumber != 0.0)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_far<true>, kFarPts * kFarLanes, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_far<false>, kFarPts * kFarLanes, 0);
+  const long long slots = (long long)sms * std::max(per_sm, 1);
+  long long chunks = std::max<long long>(1, std::min<long long>(4 * slots / tiles,
                                                                 (m + 63) / 64));
   chunks = std::min<long long>(chunks, 65535);
   const long long chunk = (m + chunks - 1) / chunks;
