@@ -1,26 +1,37 @@
-"""Far-field evaluation of the scattering application on the GPU
-(SURVEY §8f row 3): ``evaluate_far_field`` and ``evaluation_ring`` with the
-signatures, validation, warning and error classes of
-`/root/reference/pkg/src/hbem/scatter.py:94-107,362-408`.
+"""The scattering application on the GPU, with the
+signatures, validation, warnings and error classes of
+`/root/reference/pkg/src/hbem/scatter.py`:
 
-The element geometry, the densities and the point x element x rule-point
-double-layer sum all run in ``hbem_far_field`` (csrc/far.cu); there is no
-host fallback.
+* ``evaluate_far_field`` / ``evaluation_ring`` (scatter.py:94-107,362-408):
+  geometry, densities and the point x element x rule-point double-layer sum
+  run in ``hbem_far_field`` (csrc/far.cu); no host fallback.
+* ``burton_miller_solve`` (scatter.py:228-359): (1/2 M - K - eta_c D) phi =
+  M u_inc - eta_c M du_inc/dn with K (Helmholtz DLP, P1c) and the single
+  layer S (Helmholtz SLP, P1d) assembled on the device (H-matrix: lock-step
+  ACA; dense: the element-pair sweep), D = sum_j Q_j^T S Q_j - k^2 sum_j
+  P_j^T S P_j (the sparse surface-curl / normal transforms of
+  spaces.py:204-246), GMRES (solvers.py) applying K and S by device matvecs.
+  The sparse mass / transform matrices and the Krylov basis are O(N) host
+  arrays, as in the reference.
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import time
 import warnings
+from dataclasses import dataclass, field
 
 import numpy as np
+import scipy.sparse as sps
 
 from . import _lib
 from ._lib import check, lib
 from .discretization import FunctionSpace, TriangleMesh, basis_table, regular_rule
-from .errors import ConfigError
+from .errors import ConfigError, MeshError, SolverError, SpaceError
 
 NEAR_FIELD_DIAMETERS = 3.0  # scatter.py:50
+MIN_ELEMENTS_PER_WAVELENGTH = 6.0  # scatter.py:49
 
 
 def evaluation_ring(n_points: int, radius: float) -> tuple[np.ndarray, np.ndarray]:
@@ -88,3 +99,287 @@ def evaluate_far_field(mesh: TriangleMesh, space: FunctionSpace, phi: np.ndarray
     out.real = ore
     out.imag = oim
     return out
+
+
+# ---------------------------------------------------------------------------
+# Burton-Miller combined-field solve                     scatter.py:52-359
+# ---------------------------------------------------------------------------
+
+def wavenumber_from_frequency(frequency: float, sound_speed: float) -> float:
+    """k = 2 pi f / c (scatter.py:52-58)."""
+    if frequency <= 0.0 or sound_speed <= 0.0:
+        raise ConfigError(
+            f"frequency and sound speed must be > 0, got {frequency}, {sound_speed}")
+    return 2.0 * np.pi * frequency / sound_speed
+
+
+def incidence_direction(theta_deg: float) -> np.ndarray:
+    """Unit propagation direction in the xy-plane (scatter.py:87-91)."""
+    t = np.deg2rad(theta_deg)
+    return np.array([np.cos(t), np.sin(t), 0.0])
+
+
+@dataclass(frozen=True)
+class PlaneWave:
+    """u(x) = amplitude exp(i k <d, x>) (scatter.py:61-84)."""
+
+    amplitude: complex
+    direction: np.ndarray
+    wavenumber: float
+
+    def __post_init__(self):
+        d = np.array(self.direction, dtype=np.float64)
+        if d.shape != (3,):
+            raise ConfigError(f"direction must be a 3-vector, got shape {d.shape}")
+        if abs(np.linalg.norm(d) - 1.0) > 1e-12:
+            raise ConfigError(
+                f"direction must be unit length within 1e-12, |d| = {np.linalg.norm(d)!r}")
+        if self.wavenumber <= 0.0:
+            raise ConfigError(f"wavenumber must be > 0, got {self.wavenumber}")
+        d.setflags(write=False)
+        object.__setattr__(self, "direction", d)
+
+    def evaluate(self, points: np.ndarray) -> np.ndarray:
+        return self.amplitude * np.exp(1j * (points @ (self.wavenumber * self.direction)))
+
+
+def _default_aca():
+    from .hmatrix import AcaConfig
+    return AcaConfig()
+
+
+def _default_assembly():
+    from .hmatrix import AssemblyConfig
+    return AssemblyConfig()
+
+
+@dataclass(frozen=True)
+class ScatterConfig:
+    """One scattering run (scatter.py:110-166).  ``build_mesh`` makes a
+    geodesic unit sphere with 20 * 4**sphere_level triangles (the
+    reference's icosphere refinement level); Gmsh files are out of scope."""
+
+    frequency: float = 477.46482927568605  # k = 2 with c = 1500
+    sound_speed: float = 1500.0
+    sphere_level: int = 3
+    mesh_file: str | None = None
+    amplitude: float = 1.0
+    theta_inc_deg: float = 0.0
+    radius: float = 100.0
+    n_points: int = 3600
+    tol: float = 1e-5
+    restart: int = 100
+    max_iter: int | None = None
+    eta: float = 2.0
+    n_min: int = 32
+    force: bool = False
+    assembly: object = field(default_factory=_default_assembly)
+    aca: object = field(default_factory=_default_aca)
+
+    def __post_init__(self):
+        checks = ((self.frequency <= 0.0, f"frequency must be > 0, got {self.frequency}"),
+                  (self.sound_speed <= 0.0, f"sound_speed must be > 0, got {self.sound_speed}"),
+                  (self.radius <= 0.0, f"radius must be > 0, got {self.radius}"),
+                  (self.n_points < 1, f"n_points must be >= 1, got {self.n_points}"),
+                  (self.mesh_file is None and self.sphere_level < 0,
+                   f"sphere_level must be >= 0, got {self.sphere_level}"),
+                  (self.tol <= 0.0, f"tol must be > 0, got {self.tol}"),
+                  (self.restart < 1, f"restart must be >= 1, got {self.restart}"))
+        for bad, msg in checks:
+            if bad:
+                raise ConfigError(msg)
+
+    @property
+    def wavenumber(self) -> float:
+        return wavenumber_from_frequency(self.frequency, self.sound_speed)
+
+    def plane_wave(self) -> PlaneWave:
+        return PlaneWave(complex(self.amplitude), incidence_direction(self.theta_inc_deg),
+                         self.wavenumber)
+
+    def build_mesh(self) -> TriangleMesh:
+        if self.mesh_file is not None:
+            raise ConfigError("mesh files (Gmsh I/O) are out of scope; pass mesh=")
+        from .meshes import geodesic_sphere
+        return TriangleMesh(*geodesic_sphere(2 ** self.sphere_level))
+
+
+@dataclass(frozen=True)
+class SolveReport:
+    """scatter.py:169-182."""
+
+    phi: np.ndarray
+    converged: bool
+    iterations: int
+    residual: float
+    residuals: tuple
+    timings: dict
+    mode: str
+    wavenumber: float
+    n_dofs: int
+    n_elements: int
+
+
+def _element_frames(mesh: TriangleMesh):
+    """|J|, unit normals and edge vectors per element (mesh.py:344-349)."""
+    v = mesh.vertices[mesh.elements]
+    e1, e2 = v[:, 1] - v[:, 0], v[:, 2] - v[:, 0]
+    cr = np.cross(e1, e2)
+    jac = np.linalg.norm(cr, axis=1)
+    return v, jac, cr / jac[:, None]
+
+
+def _check_closed_oriented(mesh: TriangleMesh):
+    """mesh_is_closed + check_consistent_orientation: every edge is used by
+    exactly two elements, once in each direction."""
+    el = mesh.elements
+    directed = np.concatenate([el[:, [0, 1]], el[:, [1, 2]], el[:, [2, 0]]])
+    und = np.sort(directed, axis=1)
+    _, inv, cnt = np.unique(und, axis=0, return_inverse=True, return_counts=True)
+    if (cnt != 2).any():
+        raise MeshError("scattering requires a closed surface mesh")
+    fwd = directed[:, 0] < directed[:, 1]
+    per_edge = np.bincount(inv.ravel(), weights=fwd.astype(np.float64), minlength=len(cnt))
+    if (per_edge != 1.0).any():
+        raise MeshError("inconsistent element orientation across a shared edge")
+
+
+def vertex_normals(mesh: TriangleMesh) -> np.ndarray:
+    """Area-weighted outward vertex normals (scatter.py:185-194)."""
+    _, jac, nrm = _element_frames(mesh)
+    acc = np.zeros((len(mesh.vertices), 3))
+    np.add.at(acc, mesh.elements.ravel(), np.repeat(nrm * (0.5 * jac)[:, None], 3, axis=0))
+    ln = np.linalg.norm(acc, axis=1)
+    if (ln == 0.0).any():
+        raise MeshError("vertex with vanishing aggregate normal")
+    return acc / ln[:, None]
+
+
+def incident_trace(wave: PlaneWave, mesh: TriangleMesh, space: FunctionSpace):
+    """Nodal u_inc and du_inc/dn = i k <d, n_v> u_inc (scatter.py:197-211)."""
+    if space.family.value != "p1c":
+        raise SpaceError(
+            f"incident traces need the continuous P1 space, got {space.family.value}")
+    if space.mesh is not mesh:
+        raise SpaceError("space was built on a different mesh")
+    u = wave.evaluate(mesh.vertices)
+    return u, 1j * wave.wavenumber * (vertex_normals(mesh) @ wave.direction) * u
+
+
+def _resolution_guard(mesh: TriangleMesh, k: float, force: bool) -> float:
+    """scatter.py:214-225: elements per wavelength from the longest edge."""
+    v = mesh.vertices[mesh.elements]
+    h = max(float(np.linalg.norm(v[:, a] - v[:, b], axis=1).max())
+            for a, b in ((1, 0), (2, 0), (2, 1)))
+    epw = (2.0 * np.pi / k) / h
+    if epw < MIN_ELEMENTS_PER_WAVELENGTH and not force:
+        raise SolverError(
+            f"mesh resolves {epw:.2f} elements per wavelength, below the "
+            f"minimum {MIN_ELEMENTS_PER_WAVELENGTH:g}; refine the mesh or "
+            "pass force=True to proceed anyway")
+    return epw
+
+
+def _mass_p1c(space: FunctionSpace, jac: np.ndarray):
+    """Galerkin P1c mass matrix with the 3-point rule (spaces.py:183-201)."""
+    rule = regular_rule(2)
+    t = basis_table(space, rule).values
+    local = (t * rule.weights[None, :]) @ t.T
+    dm = space.dofmap
+    rows = np.repeat(dm, 3, axis=1).ravel()
+    cols = np.tile(dm, (1, 3)).ravel()
+    vals = (jac[:, None, None] * local[None]).ravel()
+    return sps.csr_matrix((vals, (rows, cols)), shape=(space.n_dofs, space.n_dofs))
+
+
+def _curl_and_normal_maps(p1c: FunctionSpace, p1d: FunctionSpace, v, jac, nrm):
+    """Q_j (surface-curl component j, constant per element, on each of the
+    element's three P1d rows) and P_j (n_j times nodal values) from P1c to
+    P1d (spaces.py:204-246)."""
+    shape = (p1d.n_dofs, p1c.n_dofs)
+    curls = np.stack([v[:, (l + 1) % 3] - v[:, (l + 2) % 3] for l in range(3)], 1)
+    curls = curls / jac[:, None, None]
+    qr = np.repeat(p1d.dofmap, 3, axis=1).ravel()
+    qc = np.tile(p1c.dofmap, (1, 3)).ravel()
+    pr, pc = p1d.dofmap.ravel(), p1c.dofmap.ravel()
+    q = [sps.csr_matrix((np.tile(curls[:, :, j], (1, 3)).ravel(), (qr, qc)), shape=shape)
+         for j in range(3)]
+    p = [sps.csr_matrix((np.repeat(nrm[:, j], 3), (pr, pc)), shape=shape) for j in range(3)]
+    return q, p
+
+
+def burton_miller_solve(cfg: ScatterConfig, wave: PlaneWave | None = None, mode: str = "dense",
+                        mesh: TriangleMesh | None = None,
+                        stats: dict | None = None) -> SolveReport:
+    """Sound-hard scattering, total surface trace phi (scatter.py:228-359),
+    with every boundary-operator application on the GPU."""
+    from .backend import make_gpu_backends
+    from .discretization import OperatorSpec, build_space, make_integration_context
+    from .hmatrix import assemble_hmatrix
+    from .partition import cluster_trees_for
+    from .solvers import gmres
+
+    if mode not in ("dense", "hmatrix"):
+        raise ConfigError(f"mode must be 'dense' or 'hmatrix', got {mode!r}")
+    wave = cfg.plane_wave() if wave is None else wave
+    k = wave.wavenumber
+    if abs(k - cfg.wavenumber) > 1e-9 * max(k, cfg.wavenumber):
+        raise ConfigError(f"wave has k = {k}, config implies k = {cfg.wavenumber}; "
+                          "they must describe the same problem")
+    mesh = cfg.build_mesh() if mesh is None else mesh
+    _check_closed_oriented(mesh)
+    epw = _resolution_guard(mesh, k, cfg.force)
+
+    t0 = time.perf_counter()
+    p1c, p1d = build_space(mesh, "p1c"), build_space(mesh, "p1d")
+    v, jac, nrm = _element_frames(mesh)
+    mass = _mass_p1c(p1c, jac)
+    qm, pm = _curl_and_normal_maps(p1c, p1d, v, jac, nrm)
+    qt, pt = [q.T.tocsr() for q in qm], [p.T.tocsr() for p in pm]
+    spec_k = OperatorSpec("helmholtz", "dlp", k)
+    spec_s = OperatorSpec("helmholtz", "slp", k)
+    if mode == "dense":
+        from .assembly import assemble_dense
+        n_dev = cfg.assembly.devices or 1
+        k_op = assemble_dense(spec_k, p1c, p1c, cfg.assembly,
+                              make_gpu_backends(make_integration_context(spec_k, p1c, p1c), n_dev))
+        s_op = assemble_dense(spec_s, p1d, p1d, cfg.assembly,
+                              make_gpu_backends(make_integration_context(spec_s, p1d, p1d), n_dev))
+        apply_k, apply_s = k_op.__matmul__, s_op.__matmul__
+    else:
+        k_op = assemble_hmatrix(spec_k, p1c, p1c, cluster_trees_for(p1c, p1c, cfg.n_min, cfg.eta),
+                                cfg.aca)
+        s_op = assemble_hmatrix(spec_s, p1d, p1d, cluster_trees_for(p1d, p1d, cfg.n_min, cfg.eta),
+                                cfg.aca)
+        apply_k, apply_s = k_op.matvec, s_op.matvec
+    eta_c = 1.0 / (1j * k)
+
+    def apply_d(x):
+        curl = np.zeros(p1c.n_dofs, np.complex128)
+        for q, qq in zip(qm, qt):
+            curl += qq @ apply_s(q @ x)
+        norm = np.zeros(p1c.n_dofs, np.complex128)
+        for p, pp in zip(pm, pt):
+            norm += pp @ apply_s(p @ x)
+        return curl - k * k * norm
+
+    def operator(x):
+        return 0.5 * (mass @ x) - apply_k(x) - eta_c * apply_d(x)
+
+    u_inc, du_inc = incident_trace(wave, mesh, p1c)
+    rhs = mass @ u_inc - eta_c * (mass @ du_inc)
+    t1 = time.perf_counter()
+    res = gmres(operator, rhs, tol=cfg.tol, restart=cfg.restart, max_iter=cfg.max_iter)
+    t2 = time.perf_counter()
+    if not res.converged:
+        err = SolverError(f"GMRES did not reach tolerance {cfg.tol:g} within "
+                          f"{res.iterations} iterations (residual {res.residual:.3e})")
+        err.residuals = res.residuals
+        raise err
+    if stats is not None:
+        stats["elements_per_wavelength"] = epw
+        stats["mode"] = mode
+    return SolveReport(phi=res.x, converged=res.converged, iterations=res.iterations,
+                       residual=res.residual, residuals=res.residuals,
+                       timings={"assembly": t1 - t0, "solve": t2 - t1}, mode=mode,
+                       wavenumber=k, n_dofs=p1c.n_dofs, n_elements=len(mesh.elements))
