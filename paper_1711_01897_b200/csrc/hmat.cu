@@ -509,6 +509,10 @@ struct hbem_hmat {
   void *mv_buf = nullptr;  // x, y, xt, yt
   int *mv_ad = nullptr;
   long long *mv_ad_l = nullptr;
+  int2 *mv_items = nullptr;       // low-rank dots items, then rows items
+  long long *mv_sbase = nullptr;  // per low-rank list position
+  void *mv_s = nullptr;
+  long long mv_nd = 0, mv_nr = 0, mv_ns = 0;
   // streamed payloads: per-wave packing of converged low-rank blocks into
   // device U / V arenas (growable), optional D2H into caller host arenas
   VPool uarena, varena;
@@ -550,6 +554,9 @@ struct hbem_hmat {
     cudaFree(mv_buf);
     cudaFree(mv_ad);
     cudaFree(mv_ad_l);
+    cudaFree(mv_items);
+    cudaFree(mv_sbase);
+    cudaFree(mv_s);
     if (mail) cudaFreeHost(mail);
     if (side) cudaStreamDestroy(side);
     if (hi) cudaStreamDestroy(hi);
@@ -1680,6 +1687,40 @@ int hbem_hmat_leaf_meta(const hbem_hmat *h, int32_t *kind, int32_t *rank, int32_
   return HBEM_OK;
 }
 
+// pack the converged low-rank factors of the last execute into the
+// contiguous U / V arenas (k_pack_factors), once: copy_arenas and the device
+// matvec read them
+int ensure_packed(hbem_hmat *h, cudaStream_t st) {
+  const size_t vb = h->vbytes;
+  if (!h->packed && h->n_lowrank > 0) {
+    const size_t n = (size_t)h->n_lowrank;
+    const int *d_slots = h->lr_list;
+    long long *d_uo = h->q_uoff, *d_vo = h->q_voff;  // free after the waves
+    k_gather_ll<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_slots, (int)n, h->blk_uoff, d_uo);
+    k_gather_ll<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_slots, (int)n, h->blk_voff, d_vo);
+    HB_CHECK(h->uarena.grow((size_t)h->u_entries * vb));
+    HB_CHECK(h->varena.grow((size_t)h->v_entries * vb));
+    const int cnt = (int)n;
+    void *ua = reinterpret_cast<void *>(h->uarena.base), *va = reinterpret_cast<void *>(h->varena.base);
+    if (h->vbytes == 16)
+      k_pack_factors<double, true><<<cnt, 128, 0, st>>>(d_slots, cnt, h->S, d_uo, d_vo, 0, 0,
+                                                           (Cx<double> *)ua, (Cx<double> *)va);
+    else if (h->vbytes == 8 && h->complex_)
+      k_pack_factors<float, true><<<cnt, 128, 0, st>>>(d_slots, cnt, h->S, d_uo, d_vo, 0, 0,
+                                                          (Cx<float> *)ua, (Cx<float> *)va);
+    else if (h->vbytes == 8)
+      k_pack_factors<double, false><<<cnt, 128, 0, st>>>(d_slots, cnt, h->S, d_uo, d_vo, 0, 0,
+                                                            (double *)ua, (double *)va);
+    else
+      k_pack_factors<float, false><<<cnt, 128, 0, st>>>(d_slots, cnt, h->S, d_uo, d_vo, 0, 0,
+                                                           (float *)ua, (float *)va);
+    HB_CUDA(cudaGetLastError());
+    HB_CUDA(cudaStreamSynchronize(st));
+    h->packed = true;
+  }
+  return HBEM_OK;
+}
+
 int hbem_hmat_copy_arenas(const hbem_hmat *hc, void *u, void *v, void *dense) {
   clear_error();
   hbem_hmat *h = const_cast<hbem_hmat *>(hc);
@@ -1720,35 +1761,12 @@ int hbem_hmat_copy_arenas(const hbem_hmat *hc, void *u, void *v, void *dense) {
     if (e != cudaSuccess) return fail(e);
   }
   // low-rank factors: packed per wave when streaming, else packed here
-  if (!h->packed && h->n_lowrank > 0) {
-    const size_t n = (size_t)h->n_lowrank;
-    const int *d_slots = h->lr_list;
-    long long *d_uo = h->q_uoff, *d_vo = h->q_voff;  // free after the waves
-    k_gather_ll<<<(unsigned)((n + 255) / 256), 256, 0, sp[0]>>>(d_slots, (int)n, h->blk_uoff, d_uo);
-    k_gather_ll<<<(unsigned)((n + 255) / 256), 256, 0, sp[0]>>>(d_slots, (int)n, h->blk_voff, d_vo);
-    if (h->uarena.grow((size_t)h->u_entries * vb) != HBEM_OK ||
-        h->varena.grow((size_t)h->v_entries * vb) != HBEM_OK) {
+  {
+    const int rc = ensure_packed(h, sp[0]);
+    if (rc != HBEM_OK) {
       done();
-      return HBEM_ERR_CAPACITY;
+      return rc;
     }
-    const int cnt = (int)n;
-    void *ua = reinterpret_cast<void *>(h->uarena.base), *va = reinterpret_cast<void *>(h->varena.base);
-    if (h->vbytes == 16)
-      k_pack_factors<double, true><<<cnt, 128, 0, sp[0]>>>(d_slots, cnt, h->S, d_uo, d_vo, 0, 0,
-                                                           (Cx<double> *)ua, (Cx<double> *)va);
-    else if (h->vbytes == 8 && h->complex_)
-      k_pack_factors<float, true><<<cnt, 128, 0, sp[0]>>>(d_slots, cnt, h->S, d_uo, d_vo, 0, 0,
-                                                          (Cx<float> *)ua, (Cx<float> *)va);
-    else if (h->vbytes == 8)
-      k_pack_factors<double, false><<<cnt, 128, 0, sp[0]>>>(d_slots, cnt, h->S, d_uo, d_vo, 0, 0,
-                                                            (double *)ua, (double *)va);
-    else
-      k_pack_factors<float, false><<<cnt, 128, 0, sp[0]>>>(d_slots, cnt, h->S, d_uo, d_vo, 0, 0,
-                                                           (float *)ua, (float *)va);
-    e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaStreamSynchronize(sp[0]);
-    if (e != cudaSuccess) return fail(e);
-    h->packed = true;
   }
   if (e == cudaSuccess && u && h->u_entries > 0)
     e = cudaMemcpyAsync(u, reinterpret_cast<const void *>(h->uarena.base),
@@ -1787,6 +1805,38 @@ int hbem_hmat_matvec(const hbem_hmat *hc, const void *x, void *y) {
       HB_CUDA(cudaMemcpy(h->mv_ad_l, h->ad_off.data(), na * 8, cudaMemcpyHostToDevice));
       HB_CUDA(cudaMemcpy(h->mv_ad_l + na, h->ad_rowbase.data(), na * 8, cudaMemcpyHostToDevice));
     }
+    // low-rank work items: (list position, chunk start) over columns (dots)
+    // and rows, kMvChunk each; per-position offsets of the k dots
+    cudaFree(h->mv_items); cudaFree(h->mv_sbase); cudaFree(h->mv_s);
+    h->mv_items = nullptr; h->mv_sbase = nullptr; h->mv_s = nullptr;
+    const int nl = h->n_lowrank;
+    std::vector<int> lst(nl), rk(h->na > 0 ? h->na : 1);
+    if (nl > 0) {
+      HB_CUDA(cudaMemcpy(lst.data(), h->lr_list, (size_t)nl * 4, cudaMemcpyDeviceToHost));
+      HB_CUDA(cudaMemcpy(rk.data(), h->S.rank, (size_t)h->na * 4, cudaMemcpyDeviceToHost));
+    }
+    std::vector<int2> items;
+    std::vector<long long> sbase(std::max(nl, 1));
+    long long ns = 0;
+    for (int p = 0; p < nl; ++p) {
+      const int b = lst[p];
+      sbase[p] = ns;
+      ns += rk[b];
+      for (int c = 0; c < h->aw[b]; c += kMvChunk) items.push_back(make_int2(p, c));
+    }
+    const long long nd_items = (long long)items.size();
+    for (int p = 0; p < nl; ++p)
+      for (int r = 0; r < h->ah[lst[p]]; r += kMvChunk) items.push_back(make_int2(p, r));
+    h->mv_nd = nd_items;
+    h->mv_nr = (long long)items.size() - nd_items;
+    h->mv_ns = ns;
+    HB_CUDA(cudaMalloc(&h->mv_items, std::max<size_t>(items.size(), 1) * sizeof(int2)));
+    HB_CUDA(cudaMalloc(&h->mv_sbase, sbase.size() * 8));
+    HB_CUDA(cudaMalloc(&h->mv_s, (size_t)std::max<long long>(ns, 1) * vb));
+    if (!items.empty())
+      HB_CUDA(cudaMemcpy(h->mv_items, items.data(), items.size() * sizeof(int2),
+                         cudaMemcpyHostToDevice));
+    HB_CUDA(cudaMemcpy(h->mv_sbase, sbase.data(), sbase.size() * 8, cudaMemcpyHostToDevice));
     h->mv_dirty = false;
   }
   MatvecArgs M{};
@@ -1805,6 +1855,18 @@ int hbem_hmat_matvec(const hbem_hmat *hc, const void *x, void *y) {
                                  h->dense_adm};
   M.n_lowrank = h->n_lowrank;
   M.lowrank = h->lr_list;
+  HB_CHECK(ensure_packed(h, 0));
+  M.ua = reinterpret_cast<const void *>(h->uarena.base);
+  M.va = reinterpret_cast<const void *>(h->varena.base);
+  M.uoff = h->blk_uoff;
+  M.voff = h->blk_voff;
+  M.n_ditems = h->mv_nd;
+  M.n_ritems = h->mv_nr;
+  M.ditems = h->mv_items;
+  M.ritems = h->mv_items + h->mv_nd;
+  M.sbase = h->mv_sbase;
+  M.s = h->mv_s;
+  M.n_s = h->mv_ns;
   HB_CUDA(cudaMemcpy(dx, x, (size_t)nc * vb, cudaMemcpyHostToDevice));
   const hbem_ctx *ctx = h->ctx;
   int rc;

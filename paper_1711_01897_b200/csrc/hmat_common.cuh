@@ -555,7 +555,19 @@ struct MatvecArgs {
   } dense[2];     // near-field leaves, admissible blocks stored densely
   int n_lowrank;
   const int *lowrank;  // admissible block slots
+  // packed factors (U h x k, V w x k per block, v = r / p applied): the
+  // matvec streams these instead of the scattered pool terms
+  const void *ua, *va;
+  const long long *uoff, *voff;  // per admissible block
+  // work items (low-rank list position, chunk start), <= kMvChunk rows or
+  // columns each, so one huge block does not serialise on one warp
+  long long n_ditems, n_ritems;
+  const int2 *ditems, *ritems;
+  const long long *sbase;  // per list position: offset of its k dots in s
+  void *s;                 // sum_k complex/real dots (zeroed per matvec)
+  long long n_s;
 };
+constexpr int kMvChunk = 512;
 template <typename T, bool C>
 int matvec_launch(const MatvecArgs &M, const AcaDev &S, cudaStream_t st);
 template <typename T, bool C>

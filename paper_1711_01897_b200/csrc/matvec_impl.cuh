@@ -1,6 +1,7 @@
 // Device H-matrix matvec y = H x (hmat_matvec, hmatrix.py:441-470) straight
 // from the device arenas: dense leaves row by row, low-rank blocks from the
-// ACA factor pool (v = r / p applied on the fly).  Leaf contributions are
+// packed U / V arenas (contiguous per block; the ACA pool scatters a block's
+// terms over one region per wave, which costs a TLB miss per term).  Leaf contributions are
 // accumulated with atomics (the sum order over leaves is not fixed, so
 // results agree with the host matvec to rounding, not bitwise).
 #pragma once
@@ -61,44 +62,86 @@ __global__ void k_mv_dense(int nl, const int *r0, const int *c0, const int *h, c
   if (lane == 0) atomic_add_v<V>(static_cast<V *>(yt) + r0[s] + i, acc);
 }
 
-// one warp per low-rank block: s_l = v_l . x, y += sum_l u_l s_l
+// one warp per low-rank block: s_l = v_l . x, y += sum_l u_l s_l.  The term
+// offsets and pivots are fetched lane-parallel (lane l holds term l) and
+// broadcast by shuffles, so every factor load is independent of the others
+// (no per-term dependent global load); dots run four terms at a time.
 template <typename T, bool C>
-__global__ void k_mv_lowrank(int n, const int *slots, AcaDev S, const void *xt, void *yt) {
+__device__ __forceinline__ typename Num<T, C>::V shfl_v(typename Num<T, C>::V v, int src) {
+  if constexpr (C) {
+    v.re = __shfl_sync(0xffffffffu, v.re, src);
+    v.im = __shfl_sync(0xffffffffu, v.im, src);
+    return v;
+  } else {
+    return __shfl_sync(0xffffffffu, v, src);
+  }
+}
+
+// low-rank blocks in two passes over (block, chunk) work items:
+//   dots: warp per (block, <= kMvChunk columns): s_l += v_l[chunk] . x[chunk]
+//   rows: warp per (block, <= kMvChunk rows):    y[chunk] += sum_l u_l[chunk] s_l
+template <typename T, bool C>
+__global__ void k_mv_dots(long long n, const int2 *items, const int *slots, AcaDev S,
+                          const void *va, const long long *voff, const long long *sbase,
+                          const void *xt, void *s) {
   using N = Num<T, C>;
   using V = typename N::V;
-  const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long it = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (q >= n) return;
-  const int b = slots[q];
-  const int h = S.h[b], w = S.w[b], k = S.rank[b];
-  const V *pool = static_cast<const V *>(S.pool);
+  if (it >= n) return;
+  const int2 wi = items[it];
+  const int b = slots[wi.x];
+  const int w = S.w[b], k = S.rank[b];
+  const int c0 = wi.y, c1 = min(w, c0 + kMvChunk);
+  const V *W = static_cast<const V *>(va) + voff[b];  // column l: W[l * w + c]
   const V *x = static_cast<const V *>(xt) + S.c0[b];
+  V *sd = static_cast<V *>(s) + sbase[wi.x];
+  for (int l = 0; l < k; l += 4) {
+    V acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] = N::zero();
+    for (int c = c0 + lane; c < c1; c += 32) {
+      const V xc = x[c];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (l + u < k) acc[u] = N::fma_acc(acc[u], W[(long long)(l + u) * w + c], xc);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const V d = warp_sum_v<T, C>(acc[u]);
+      if (lane == 0 && l + u < k) atomic_add_v<V>(sd + l + u, d);
+    }
+  }
+}
+
+template <typename T, bool C>
+__global__ void k_mv_rows(long long n, const int2 *items, const int *slots, AcaDev S,
+                          const void *ua, const long long *uoff, const long long *sbase,
+                          const void *s, void *yt) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  const long long it = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (it >= n) return;
+  const int2 wi = items[it];
+  const int b = slots[wi.x];
+  const int h = S.h[b], k = S.rank[b];
+  const int r0 = wi.y, r1 = min(h, r0 + kMvChunk);
+  const V *U = static_cast<const V *>(ua) + uoff[b];  // column l: U[l * h + i]
+  const V *sd = static_cast<const V *>(s) + sbase[wi.x];
   V *y = static_cast<V *>(yt) + S.r0[b];
-  const long long *tl = S.terms + (long long)b * S.tmax;
   for (int l0 = 0; l0 < k; l0 += 32) {
     const int lk = min(32, k - l0);
-    V mine = N::zero();
-    for (int l = 0; l < lk; ++l) {
-      const V *t = pool + tl[l0 + l];
-      V acc = N::zero();
-      for (int c = lane; c < w; c += 32) acc = N::fma_acc(acc, t[h + c], x[c]);
-      acc = warp_sum_v<T, C>(acc);
-      if (lane == l) mine = N::div(acc, t[h + w]);
-    }
-    for (int i0 = 0; i0 < h; i0 += 32) {  // warp-uniform trip count (shuffles below)
+    const V mine = lane < lk ? sd[l0 + lane] : N::zero();
+    for (int i0 = r0; i0 < r1; i0 += 32) {  // warp-uniform trip count (shuffles)
       const int i = i0 + lane;
       V acc = N::zero();
+#pragma unroll 4
       for (int l = 0; l < lk; ++l) {
-        V sl;
-        if constexpr (C) {
-          sl.re = __shfl_sync(0xffffffffu, mine.re, l);
-          sl.im = __shfl_sync(0xffffffffu, mine.im, l);
-        } else {
-          sl = __shfl_sync(0xffffffffu, mine, l);
-        }
-        if (i < h) acc = N::fma_acc(acc, pool[tl[l0 + l] + i], sl);
+        const V sl = shfl_v<T, C>(mine, l);
+        if (i < r1) acc = N::fma_acc(acc, U[(long long)(l0 + l) * h + i], sl);
       }
-      if (i < h) atomic_add_v<V>(y + i, acc);
+      if (i < r1) atomic_add_v<V>(y + i, acc);
     }
   }
 }
@@ -128,9 +171,13 @@ int matvec_launch(const MatvecArgs &M, const AcaDev &S, cudaStream_t st) {
     k_mv_dense<T, C><<<(unsigned)((warps + 3) / 4), 128, 0, st>>>(
         D.n, D.r0, D.c0, D.h, D.w, D.off, D.rowbase, D.nrows, D.arena, M.xt, M.yt);
   }
-  if (M.n_lowrank > 0)
-    k_mv_lowrank<T, C><<<(unsigned)((M.n_lowrank + 3) / 4), 128, 0, st>>>(M.n_lowrank, M.lowrank,
-                                                                         S, M.xt, M.yt);
+  if (M.n_lowrank > 0) {
+    HB_CUDA(cudaMemsetAsync(M.s, 0, (size_t)std::max<long long>(M.n_s, 1) * vb, st));
+    k_mv_dots<T, C><<<(unsigned)((M.n_ditems + 3) / 4), 128, 0, st>>>(
+        M.n_ditems, M.ditems, M.lowrank, S, M.va, M.voff, M.sbase, M.xt, M.s);
+    k_mv_rows<T, C><<<(unsigned)((M.n_ritems + 3) / 4), 128, 0, st>>>(
+        M.n_ritems, M.ritems, M.lowrank, S, M.ua, M.uoff, M.sbase, M.s, M.yt);
+  }
   k_mv_scatter<T, C><<<(M.n_rows + 255) / 256, 256, 0, st>>>(M.n_rows, M.rperm, M.yt, M.y);
   HB_CUDA(cudaGetLastError());
   return HBEM_OK;
