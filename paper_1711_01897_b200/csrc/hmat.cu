@@ -230,10 +230,10 @@ __global__ void k_emit_offsets(const int *list, int n, const longlong2 *scan,
   q_voff[p] = vo;
 }
 
-// small device -> host reads (phase totals, counters) by a one-warp kernel
-// storing into the mapped page-locked mailbox: a cudaMemcpyAsync D2H would
-// queue on the copy engine behind the multi-GB payload copies and stall the
-// wave loop on them
+// small device -> host reads (phase totals, counters) while payloads stream:
+// a one-warp kernel stores into the mapped page-locked mailbox, because a
+// cudaMemcpyAsync D2H would queue on the copy engine behind the multi-GB
+// payload copies and stall the wave loop on them
 struct MailCopy {
   const unsigned *src[3];
   unsigned *dst[3];
@@ -468,6 +468,14 @@ struct hbem_hmat {
   char *mail_dev = nullptr;  // device view of the mailbox
   // D2H of up to three small device ranges into mailbox fields (k_mail)
   int read_mail(cudaStream_t st, std::initializer_list<std::tuple<void *, const void *, size_t>> r) {
+    if (!streaming()) {
+      // copy engine idle: plain D2H (a kernel would wait for an SM slot
+      // behind the low-priority near-field CTAs, ~ms per phase)
+      for (const auto &[dst, src, bytes] : r)
+        HB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+      HB_CUDA(cudaStreamSynchronize(st));
+      return HBEM_OK;
+    }
     MailCopy m{};
     int i = 0;
     for (const auto &[dst, src, bytes] : r) {
