@@ -340,13 +340,18 @@ def run_ours(args):
                 "achieved": flop_rate / 1e12, "peak": peak.value / 1e12, "unit": "TFLOP/s",
                 "frac": flop_rate / peak.value if peak.value else None,
                 "traffic": _ncu_traffic(),
-                "peak_source": "measured live on this GPU: hbem_probe_fma (independent DFMA "
-                               "chains, 2 FLOP per FMA); MEASURED_PEAKS.json has no FP64 figure",
+                "peak_source": ("measured live on this GPU: hbem_probe_fma (independent "
+                                f"{'DFMA' if args.precision == 'double' else 'FFMA'} chains, "
+                                "2 FLOP per FMA); MEASURED_PEAKS.json has no FP64/FP32 FMA "
+                                "figure"),
                 "algorithmic": f"{FLOP_PER_PAIR_LAP_SLP_P0} FLOP per regular pair (SURVEY 8d) x "
                                f"{aca_entries // max(args.steps, 1)} ACA entries per step",
-                "issue_frac": dp_issue / (peak.value / 2) if peak.value else None,
-                "issue_model": f"{DP_INSTR_PER_PAIR} FP64 instructions per pair (12 per "
-                               "quadrature-point pair, from cuobjdump -sass) / FP64 lane rate",
+                # the SASS instruction count is the FP64 kernel's
+                "issue_frac": (dp_issue / (peak.value / 2)
+                               if peak.value and args.precision == "double" else None),
+                "issue_model": (f"{DP_INSTR_PER_PAIR} FP64 instructions per pair (12 per "
+                                "quadrature-point pair, from cuobjdump -sass) / FP64 lane rate"
+                                if args.precision == "double" else None),
                 "launches_per_step": int_launches // max(args.steps, 1),
                 "avg_launch_ms": int_ms / max(int_launches, 1),
                 "int_kernel_ms_per_step": int_ms / max(args.steps, 1),
