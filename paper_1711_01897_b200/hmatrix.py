@@ -165,11 +165,17 @@ class _DevicePart:
         # assembler reads it on re-execute and matvec reads its precision
         self.context = context
         self.dtype = dtype
-        self.shapes = shapes  # (L, 2) h, w
+        self._shapes = shapes  # (L, 2) h, w, or a callable computing them on first use
         self.n_leaves = n_leaves
         self._pinned = []
         self._lock = threading.Lock()
         self._refresh()
+
+    @property
+    def shapes(self) -> np.ndarray:
+        if callable(self._shapes):
+            self._shapes = self._shapes()
+        return self._shapes
 
     def _refresh(self):
         L, handle = self.n_leaves, self.handle
@@ -381,7 +387,10 @@ def _assemble_part(dev_ctx, tree: BlockClusterTree, leaf_ids, test_space, trial_
     arrays of the result dtype: the payloads are streamed into them while the
     assembly runs (hbem_hmat_desc.out_*), wave by wave."""
     rows, cols = tree.rows, tree.cols
-    la = np.ascontiguousarray(tree.leaf_array[leaf_ids])
+    la = tree.leaf_array
+    if not (len(leaf_ids) == len(la) and np.array_equal(leaf_ids, np.arange(len(la)))):
+        la = la[leaf_ids]
+    la = np.ascontiguousarray(la, np.int64)
     keep = [la]
     d = _lib.HmatDesc()
     rp = np.ascontiguousarray(rows.permutation, np.int64)
@@ -411,7 +420,10 @@ def _assemble_part(dev_ctx, tree: BlockClusterTree, leaf_ids, test_space, trial_
         d.out_u_cap, d.out_v_cap, d.out_dense_cap = (len(a) for a in out)
     h = C.c_void_p()
     check(lib.hbem_hmat_assemble(dev_ctx.handle, C.byref(d), stream, C.byref(h)))
-    shapes = np.stack([rn[la[:, 0], 1] - rn[la[:, 0], 0], cn[la[:, 1], 1] - cn[la[:, 1], 0]], 1)
+    def shapes():  # leaf (h, w), only needed for host payload views
+        rsz, csz = rn[:, 1] - rn[:, 0], cn[:, 1] - cn[:, 0]
+        return np.stack([rsz[la[:, 0]], csz[la[:, 1]]], 1)
+
     part = _DevicePart(h, len(la), shapes, dev_ctx.spec.result_dtype, n_rows=len(rp),
                        context=dev_ctx)
     if out is not None:
