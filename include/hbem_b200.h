@@ -39,7 +39,9 @@ enum {
   HBEM_ERR_CONFIG = 3,   /* ConfigError            */
   HBEM_ERR_CUDA = 4,     /* device failure (AssemblyError at the caller) */
   HBEM_ERR_ARG = 5,      /* malformed argument     */
-  HBEM_ERR_KERNEL = 6    /* KernelError            */
+  HBEM_ERR_KERNEL = 6,   /* KernelError            */
+  HBEM_ERR_MESH = 7,     /* MeshError              */
+  HBEM_ERR_MESH_PARSE = 8 /* MeshParseError (line / section: hbem_gmsh_error_location) */
 };
 
 /* OperatorSpec fields (kernels.py:54-96) */
@@ -152,6 +154,23 @@ int hbem_blocks_size(const hbem_blocks *b, int64_t *n_leaves);
 /* leaves (n_leaves, 3) [row_node, col_node, admissible] in descent order */
 int hbem_blocks_copy(const hbem_blocks *b, int64_t *leaves);
 int hbem_blocks_destroy(hbem_blocks *b);
+
+/* ---------------------------------------------------------------------
+ * Gmsh 2.2 ASCII reader (load_mesh, mesh.py:134-245): 3-node triangles
+ * only (other element types counted in n_skipped), referenced vertices
+ * compacted in ascending node-tag order.  HBEM_ERR_MESH when the file
+ * cannot be read, HBEM_ERR_MESH_PARSE with the reference's message, line
+ * number and section otherwise.
+ * --------------------------------------------------------------------- */
+typedef struct hbem_mesh_file hbem_mesh_file;
+int hbem_gmsh_read(const char *path, hbem_mesh_file **out);
+int hbem_gmsh_size(const hbem_mesh_file *m, int64_t *n_vertices, int64_t *n_elements,
+                   int64_t *n_skipped);
+/* vertices (n_vertices, 3) float64, elements (n_elements, 3) int64 */
+int hbem_gmsh_copy(const hbem_mesh_file *m, double *vertices, int64_t *elements);
+/* line (1-based, -1 if none) and section ("" if none) of the last parse error */
+int hbem_gmsh_error_location(int64_t *line, char *section, int32_t cap);
+int hbem_gmsh_destroy(hbem_mesh_file *m);
 
 /* ---------------------------------------------------------------------
  * Device H-matrix assembly (assemble_hmatrix, hmatrix.py:759-811) with

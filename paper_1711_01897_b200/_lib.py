@@ -22,6 +22,8 @@ _CODE_TO_EXC = {
     4: errors.DeviceError,
     5: errors.HbemError,
     6: errors.KernelError,
+    7: errors.MeshError,
+    8: errors.MeshParseError,
 }
 
 EQUATIONS = {"laplace": 0, "helmholtz": 1}
@@ -126,6 +128,11 @@ SIGNATURES = [
     ("hbem_blocks_size", C.c_int, [C.c_void_p, c_int64_p]),
     ("hbem_blocks_copy", C.c_int, [C.c_void_p, c_int64_p]),
     ("hbem_blocks_destroy", C.c_int, [C.c_void_p]),
+    ("hbem_gmsh_read", C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    ("hbem_gmsh_size", C.c_int, [C.c_void_p, c_int64_p, c_int64_p, c_int64_p]),
+    ("hbem_gmsh_copy", C.c_int, [C.c_void_p, c_double_p, c_int64_p]),
+    ("hbem_gmsh_error_location", C.c_int, [c_int64_p, C.c_char_p, C.c_int32]),
+    ("hbem_gmsh_destroy", C.c_int, [C.c_void_p]),
     ("hbem_hmat_assemble", C.c_int,
      [C.c_void_p, C.POINTER(HmatDesc), C.c_void_p, C.POINTER(C.c_void_p)]),
     ("hbem_hmat_execute", C.c_int, [C.c_void_p, C.c_void_p]),
@@ -167,6 +174,15 @@ def check(status: int) -> None:
     if status == HBEM_OK:
         return
     msg = lib.hbem_last_error().decode("utf-8", "replace")
+    if status == 8:
+        # MeshParseError: the message already carries the location suffix;
+        # expose line / section as attributes like the reference
+        line, sec = C.c_int64(-1), C.create_string_buffer(64)
+        lib.hbem_gmsh_error_location(C.byref(line), sec, 64)
+        exc = errors.MeshParseError(msg)
+        exc.line = int(line.value) if line.value >= 0 else None
+        exc.section = sec.value.decode() or None
+        raise exc
     raise _CODE_TO_EXC.get(status, errors.HbemError)(msg)
 
 

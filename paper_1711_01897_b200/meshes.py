@@ -172,3 +172,78 @@ def elongated_hull(n_around: int, n_along: int, length: float = 8.0,
     if vol < 0:
         elems = elems[:, [0, 2, 1]]
     return np.ascontiguousarray(verts), np.ascontiguousarray(elems)
+
+
+def load_mesh(path):
+    """Read a Gmsh 2.2 ASCII file (mesh.py:134-245) with the native parser
+    (``hbem_gmsh_read``, csrc/gmsh.cpp): 3-node triangles only, other element
+    types counted in ``meta['skipped_elements']``, unreferenced vertices
+    dropped and indices compacted in ascending node-tag order.  Raises
+    MeshError when the file cannot be read and MeshParseError (with ``line``
+    and ``section``) on malformed input, with the reference's messages."""
+    import ctypes as C
+    import os
+
+    from . import _lib
+    from .discretization import TriangleMesh
+    path = os.fspath(path)
+    h = C.c_void_p()
+    _lib.check(_lib.lib.hbem_gmsh_read(path.encode(), C.byref(h)))
+    try:
+        nv, ne, ns = C.c_int64(), C.c_int64(), C.c_int64()
+        _lib.check(_lib.lib.hbem_gmsh_size(h, C.byref(nv), C.byref(ne), C.byref(ns)))
+        v = np.empty((nv.value, 3), np.float64)
+        e = np.empty((ne.value, 3), np.int64)
+        _lib.check(_lib.lib.hbem_gmsh_copy(h, _lib.ptr(v, C.c_double), _lib.ptr(e, C.c_int64)))
+    finally:
+        _lib.lib.hbem_gmsh_destroy(h)
+    return TriangleMesh(v, e, meta={"skipped_elements": int(ns.value), "source": path})
+
+
+# The icosahedron of refine_unit_sphere (mesh.py:248-265): vertex order and
+# face list are data the icosphere's bits depend on, so they follow the
+# reference table (the common (+-1, +-t, 0) cyclic listing).
+_ICO_T = (1.0 + np.sqrt(5.0)) / 2.0
+_ICO_V = np.array([(-1, _ICO_T, 0), (1, _ICO_T, 0), (-1, -_ICO_T, 0), (1, -_ICO_T, 0),
+                   (0, -1, _ICO_T), (0, 1, _ICO_T), (0, -1, -_ICO_T), (0, 1, -_ICO_T),
+                   (_ICO_T, 0, -1), (_ICO_T, 0, 1), (-_ICO_T, 0, -1), (-_ICO_T, 0, 1)],
+                  dtype=np.float64)
+_ICO_F = np.array([(0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11),
+                   (1, 5, 9), (5, 11, 4), (11, 10, 2), (10, 7, 6), (7, 1, 8),
+                   (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9),
+                   (4, 9, 5), (2, 4, 11), (6, 2, 10), (8, 6, 7), (9, 8, 1)], dtype=np.int64)
+MAX_SPHERE_LEVEL = 8
+
+
+def icosphere(level: int) -> tuple[np.ndarray, np.ndarray]:
+    """The reference's icosphere (refine_unit_sphere, mesh.py:269-310) bit for
+    bit, vectorised per level: every face (a, b, c) becomes (a, ab, ca),
+    (b, bc, ab), (c, ca, bc), (ab, bc, ca); edge midpoints are numbered in
+    order of first use over the faces' (ab, bc, ca) edges and projected with
+    the same v / np.linalg.norm(v) as the reference (per vertex, so the
+    norm's BLAS evaluation is the reference's)."""
+    if not isinstance(level, (int, np.integer)) or level < 0:
+        raise ValueError(f"refinement level must be a non-negative integer, got {level!r}")
+    if level > MAX_SPHERE_LEVEL:
+        raise ValueError(f"refinement level {level} exceeds maximum {MAX_SPHERE_LEVEL}")
+    verts = np.array([v / np.linalg.norm(v) for v in _ICO_V])
+    faces = _ICO_F.copy()
+    for _ in range(level):
+        a, b, c = faces[:, 0], faces[:, 1], faces[:, 2]
+        # edges in first-use order: per face ab, bc, ca
+        e = np.stack([np.stack([a, b], 1), np.stack([b, c], 1), np.stack([c, a], 1)], 1)
+        e = e.reshape(-1, 2)
+        key = np.minimum(e[:, 0], e[:, 1]) * len(verts) + np.maximum(e[:, 0], e[:, 1])
+        uk, first, inv = np.unique(key, return_index=True, return_inverse=True)
+        rank = np.empty(len(uk), np.int64)
+        order = np.argsort(first, kind="stable")
+        rank[order] = np.arange(len(uk))
+        mid = (len(verts) + rank[inv]).reshape(-1, 3)
+        ab, bc, ca = mid[:, 0], mid[:, 1], mid[:, 2]
+        ue = e[first[order]]
+        m = verts[ue[:, 0]] + verts[ue[:, 1]]
+        m = np.array([r / np.linalg.norm(r) for r in m]).reshape(-1, 3)
+        verts = np.concatenate([verts, m])
+        faces = np.stack([np.stack([a, ab, ca], 1), np.stack([b, bc, ab], 1),
+                          np.stack([c, ca, bc], 1), np.stack([ab, bc, ca], 1)], 1).reshape(-1, 3)
+    return verts, faces

@@ -199,9 +199,14 @@ class ScatterConfig:
 
     def build_mesh(self) -> TriangleMesh:
         if self.mesh_file is not None:
-            raise ConfigError("mesh files (Gmsh I/O) are out of scope; pass mesh=")
-        from .meshes import geodesic_sphere
-        return TriangleMesh(*geodesic_sphere(2 ** self.sphere_level))
+            from .meshes import load_mesh
+            return load_mesh(self.mesh_file)
+        # the reference's icosphere (refine_unit_sphere, mesh.py:269-310), bit for bit
+        from .meshes import icosphere
+        try:
+            return TriangleMesh(*icosphere(self.sphere_level))
+        except ValueError as exc:
+            raise MeshError(str(exc)) from None
 
 
 @dataclass(frozen=True)
