@@ -21,8 +21,10 @@ Arms:
   --impl reference the reference algorithm on the host CPU cores: the CPU
                    oracle (numpy restatement, oracle/hbem_oracle.py; the
                    reference is pure Python/numpy so there is no compiled
-                   oracle/_ref) assembling a cost-weighted random sample of the
-                   same leaves with one process per core.
+                   oracle/_ref) with its own numpy partition, assembling a
+                   uniform random sample of the C5 leaves with one process per
+                   core, plus one complete C1 assembly on one core.  No product
+                   native code is loaded on this arm.
 """
 
 from __future__ import annotations
@@ -193,21 +195,17 @@ def _oracle_worker(arg):
     return _oracle_leaves(ids, seconds)
 
 
-def cpu_sample_ids(bt, n, rng):
-    from paper_1711_01897_b200.hmatrix import _leaf_costs
-    cost = _leaf_costs(bt)
-    p = cost / cost.sum()
-    return rng.choice(len(cost), size=min(n, len(cost)), replace=False, p=p)
-
-
-def cpu_rate(bt, seconds, workers, rng):
-    """Assemble cost-weighted random leaves for about ``seconds`` per worker
-    (every worker stops after its time budget); returns (pairs/s, regular,
-    singular, leaves, wall) with wall = the slowest worker."""
-    ids = cpu_sample_ids(bt, 200000, rng)
+def cpu_rate(n_leaves, seconds, workers, rng):
+    """Assemble uniformly drawn leaves (an unbiased sample of the assembly's
+    per-leaf work: most C5 leaves are small, and small leaves pay the
+    reference's per-block host overhead) for about ``seconds`` per worker;
+    returns (pairs/s, regular, singular, leaves, wall, est_single_core_s)
+    with wall = the slowest worker and est_single_core_s = the whole
+    assembly's single-core time extrapolated from the mean time per leaf."""
+    ids = rng.permutation(n_leaves)[:200000]
     if workers <= 1:
         wall, reg, sing, done = _oracle_leaves(ids, seconds)
-        return (reg + sing) / wall, reg, sing, done, wall
+        return (reg + sing) / wall, reg, sing, done, wall, wall / done * n_leaves
     import multiprocessing as mp
     ctx = mp.get_context("fork")
     chunks = [(ids[i::workers], seconds) for i in range(workers)]
@@ -216,37 +214,91 @@ def cpu_rate(bt, seconds, workers, rng):
     wall = max(x[0] for x in res)
     reg = sum(x[1] for x in res)
     sing = sum(x[2] for x in res)
-    return (reg + sing) / wall, reg, sing, sum(x[3] for x in res), wall
+    done = sum(x[3] for x in res)
+    busy = sum(x[0] for x in res)
+    return (reg + sing) / wall, reg, sing, done, wall, busy / done * n_leaves
+
+
+def oracle_partition(v, e):
+    """The reference's partition restated in numpy (oracle.cluster_tree /
+    block_tree, hmatrix.py:105-211; bit-identical to the reference's, pinned
+    by tests/test_oracle_golden.py and tests/test_partition_scale.py)."""
+    from oracle import hbem_oracle as O
+    P = O.Problem(O.Spec("laplace", "slp"), v, e, "p0", "p0")
+    tree = O.cluster_tree(P.dof_centers("p0"))
+    return tree, O.block_tree(tree, tree)
+
+
+def oracle_complete_c1(eps, precision):
+    """One COMPLETE assembly of C1 (geodesic sphere n=11, 2 420 triangles,
+    Laplace SLP P0, the reference's CPU-runnable config) with the oracle on
+    one core: every leaf, ACA + near field."""
+    from oracle import hbem_oracle as O
+    from paper_1711_01897_b200.meshes import geodesic_sphere
+    v, e = geodesic_sphere(11)
+    P = O.Problem(O.Spec("laplace", "slp", 0.0, precision), v, e, "p0", "p0")
+    tree = O.cluster_tree(P.dof_centers("p0"))
+    leaves = O.block_tree(tree, tree)
+    t0 = time.perf_counter()
+    asm = O.Assembler(P, tree, tree, leaves, eps)
+    asm.assemble()
+    wall = time.perf_counter() - t0
+    pairs = asm.counters["regular_pairs"] + asm.counters["singular_pairs"]
+    return {"config": "C1: geodesic sphere n=11 (2420 triangles), Laplace SLP P0, "
+                      f"eps={eps:g}, {precision}, every leaf", "seconds": wall,
+            "regular_pairs": asm.counters["regular_pairs"],
+            "singular_pairs": asm.counters["singular_pairs"],
+            "value": pairs / wall, "unit": UNIT, "cores": 1}
 
 
 def run_reference(args):
+    """The reference's CPU path: the oracle (numpy restatement of
+    hbem.hmatrix.assemble_hmatrix's per-leaf path: aca/_row_job/_col_job/
+    dense_leaf + integrate_batch + local_matrix) over the same C5 mesh, with
+    the oracle's own partition.  Nothing from the product package runs here
+    except the synthetic mesh generator (pure numpy)."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    v, e, mesh, sp, bt, spec = workload(args)
+    from paper_1711_01897_b200.meshes import geodesic_sphere
+    v, e = geodesic_sphere(args.n)
     cores = os.cpu_count() or 1
-    _oracle_setup(v, e, bt, args.eps, args.precision)
+    t0 = time.perf_counter()
+    tree, leaves = oracle_partition(v, e)
+    t_part = time.perf_counter() - t0
+    from oracle import hbem_oracle as O
+    P = O.Problem(O.Spec("laplace", "slp", 0.0, args.precision), v, e, "p0", "p0")
+    _G["asm"] = O.Assembler(P, tree, tree, leaves, args.eps)
+    c1 = oracle_complete_c1(args.eps, args.precision)
     rng = np.random.default_rng(1234)
-    per_step = max(2.0, min(args.cpu_seconds, 20.0))
+    # the whole --steps/--warmup run stays within a few minutes
+    per_step = float(np.clip(240.0 / max(args.steps + args.warmup / 4, 1), 2.0, args.cpu_seconds))
     for _ in range(args.warmup):
-        cpu_rate(bt, min(per_step / 4, 2.0), cores, rng)
-    rates, times = [], []
+        cpu_rate(len(leaves), min(per_step / 4, 2.0), cores, rng)
+    rates, times, est = [], [], []
     for _ in range(args.steps):
-        rate, reg, sing, nl, wall = cpu_rate(bt, per_step, cores, rng)
+        rate, reg, sing, nl, wall, est_s = cpu_rate(len(leaves), per_step, cores, rng)
         rates.append(rate)
         times.append(wall)
+        est.append(est_s)
     rate = float(np.median(rates))
-    sample = (f"{nl} leaves per step ({per_step:g} s per process) drawn cost-weighted from the "
-              f"{len(bt.leaf_array)} C5 leaves; oracle (numpy restatement of hbem.hmatrix.aca/_row_job/_col_job/"
-              f"dense_leaf + integrate_batch + local_matrix) on {cores} processes")
+    assert "paper_1711_01897_b200._lib" not in sys.modules  # no product native code here
+    sample = (f"{nl} leaves per step ({per_step:.1f} s per process) drawn uniformly from the "
+              f"{len(leaves)} C5 leaves (oracle partition, {t_part:.0f} s); oracle on {cores} "
+              "processes (the reference is single-threaded Python: one process per core)")
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * float(np.median(times)), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.precision == "double" else "f32",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if args.precision == "double" else "f32",
             "data": "synthetic geodesic sphere", "config": config(args, world),
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": sample},
+                             "sample": sample,
+                             "extrapolated_c5_assembly_s_single_core": float(np.median(est)),
+                             "extrapolated_c5_assembly_s_all_cores": float(np.median(est)) / cores,
+                             "partition_s": t_part},
+            "complete_c1": c1,
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -361,11 +413,12 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         _oracle_setup(v, e, bt, args.eps, args.precision)
-        rate, reg, sg, nl, wall = cpu_rate(bt, args.cpu_seconds, 1, np.random.default_rng(7))
+        rate, reg, sg, nl, wall, est = cpu_rate(len(bt.leaf_array), args.cpu_seconds, 1,
+                                                np.random.default_rng(7))
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"{nl} C5 leaves drawn cost-weighted ({reg} regular + {sg} singular "
+               "sample": f"{nl} C5 leaves drawn uniformly ({reg} regular + {sg} singular "
                          f"pairs in {wall:.1f} s), oracle on 1 core",
-               "extrapolated_assembly_s": (stats["regular_pairs"] + stats["singular_pairs"]) / rate}
+               "extrapolated_assembly_s": est}
         # release the oracle's millions of Python objects before the e2e
         # timing (the cyclic GC would otherwise scan them mid-measurement)
         import gc

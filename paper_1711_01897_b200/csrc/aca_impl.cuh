@@ -25,16 +25,18 @@
 #pragma once
 #include <cub/cub.cuh>
 
+#include <type_traits>
+
 #include "hmat_common.cuh"
 
 namespace hb {
 
 constexpr unsigned kFull = 0xffffffffu;
-#ifndef HB_JOB_GROUP
-#define HB_JOB_GROUP 2  // jobs whose quadratures run interleaved in k_aca_p0 (2 or 4)
+#ifndef HB_ACA_P0_MINB
+#define HB_ACA_P0_MINB 4  // k_aca_p0 resident CTAs per SM (register cap 128)
 #endif
-#ifndef HB_EXPERIMENT
-#define HB_EXPERIMENT 0  // timing experiments only (bit 1: no tile argmax, 2: no dots, 4: no residual)
+#ifndef HB_JOB_GROUP
+#define HB_JOB_GROUP 1  // jobs whose quadratures run interleaved in k_aca_p0 (1 or 2)
 #endif
 
 // ---------------------------------------------------------------------------
@@ -89,9 +91,8 @@ __global__ void k_need(AcaDev S, int na, int col, int NT_, int NS_) {
       head = key != (col ? S.rnode[bp] : S.cnode[bp]);
     }
     d.pool = (!col && S.pend[b] < 0) ? (long long)h + w + 1 : 0;
-    // statistics (4 per tile) + dots (k NC per tile), padded even so every
-    // job's records start 16-byte aligned
-    d.part = ((long long)tiles * k * NC + 1) & ~1ll;
+    // per tile: statistics (4) + dots (k NC), padded even (part_len)
+    d.part = (long long)tiles * part_len(k, NC);
     d.items = head ? tiles : 0;
     if (NT_ != 1 || NS_ != 1) {
       // element-level rows: the varying cluster's element union
@@ -240,8 +241,9 @@ struct JobS {
   long long pe;     // pending record
   long long part;   // first tile record
   long long rsc_off;  // element-row values (linear spaces)
-  long long mofs;   // mask word base of the varying side
   int b, h, w, k, fix, cur;
+  unsigned mw;      // used-index mask word of the varying side at this tile
+  int pad_;
 };
 
 // ---------------------------------------------------------------------------
@@ -252,7 +254,11 @@ struct JobS {
 //   row:    val = A(i, c) - sum_l u_l[i] v_l[c]   (hmatrix.py:323-327)
 //   column: val = A(r, j) - sum_l v_l[j] u_l[r]   (hmatrix.py:340-342)
 // Writes the residual into the pending record and the tile record
-// [best |val| over unmasked, its index, sum |val|^2, vdot(f_l, val) ...].
+// [best |val| over unmasked, its index, sum |val|^2, pad, vdot(f_l, val) ...]:
+// the pivot statistics of the residual (argmax over unused indices, first
+// index on ties, hmatrix.py:301-314 / 329-332; squared norm 343-362) are
+// reduced here while the values are in registers, so the finalize kernels
+// never re-read the residual rows and columns.
 // ---------------------------------------------------------------------------
 template <typename T, bool C, bool COL>
 __device__ __forceinline__ void aca_epi(const AcaDev &S, const JobS &J, const V_t<T, C> *cs,
@@ -268,7 +274,7 @@ __device__ __forceinline__ void aca_epi(const AcaDev &S, const JobS &J, const V_
   // f_l at this lane's entry: fb[l * 32 + lane] (valid lanes only)
 #pragma unroll
   for (int l = 0; l < kFinRegs; ++l)
-    if (!(HB_EXPERIMENT & 4) && l < kk && valid) val = N::fms(val, cs[l], fb[l * 32 + lane]);
+    if (l < kk && valid) val = N::fms(val, cs[l], fb[l * 32 + lane]);
   // terms beyond the register batch (late waves of high-rank blocks)
   const long long *tl = S.terms + (long long)J.b * S.tmax;
   const int fixo = COL ? J.h + J.fix : J.fix;
@@ -278,12 +284,22 @@ __device__ __forceinline__ void aca_epi(const AcaDev &S, const JobS &J, const V_
     if (valid) val = N::fms(val, c, pool[tb + ro + idx]);
   }
   if (valid) pool[J.pe + (COL ? 0 : J.h) + idx] = val;
-  // dot records of this tile: k (x2 complex) values at rec[3 + l NC]
-  const int nt = tiles_of(COL ? J.h : J.w);
-  (void)nt;
-  double *rec = S.part + J.part + (long long)t * k * NC - 3;
+  double *rec = S.part + J.part + (long long)t * part_len(k, NC);
+  {
+    // column phase: the block's current row is excluded from the next pivot
+    const bool masked = !valid || ((J.mw >> lane) & 1u) || (COL && idx == J.cur);
+    double best = masked ? -1.0 : N::abs(val);
+    int bidx = masked ? 0x7fffffff : idx;
+    double ss = valid ? N::nrm(val) : 0.0;
+    warp_argmax_sum(best, bidx, ss);
+    if (lane == 0) {
+      rec[0] = best;
+      rec[1] = (double)bidx;
+      rec[2] = ss;
+    }
+  }
   // dots vdot(f_l, val) of the register batch: transposed reduction
-  if (!(HB_EXPERIMENT & 2) && kk > 0) {
+  if (kk > 0) {
     double dr[8], di[8];
 #pragma unroll
     for (int l = 0; l < 8; ++l) {
@@ -295,8 +311,8 @@ __device__ __forceinline__ void aca_epi(const AcaDev &S, const JobS &J, const V_
     const double si = C ? tr_reduce8(di, lane) : 0.0;
     const int l = lane >> 2;
     if ((lane & 3) == 0 && l < kk) {
-      rec[3 + l * NC] = sr;
-      if (C) rec[3 + l * NC + 1] = si;
+      rec[4 + l * NC] = sr;
+      if (C) rec[4 + l * NC + 1] = si;
     }
   }
   for (int l = kFinRegs; l < k; ++l) {
@@ -306,23 +322,24 @@ __device__ __forceinline__ void aca_epi(const AcaDev &S, const JobS &J, const V_
     dr = warp_sum_d(dr);
     if (C) di = warp_sum_d(di);
     if (lane == 0) {
-      rec[3 + l * NC] = dr;
-      if (C) rec[3 + l * NC + 1] = di;
+      rec[4 + l * NC] = dr;
+      if (C) rec[4 + l * NC + 1] = di;
     }
   }
 }
 
 // stage job p (lane-level) into shared memory; returns false past the group
 template <typename T, bool C, bool COL>
-__device__ __forceinline__ bool stage_job(const AcaDev &S, int p, int n, int key0, JobS &js,
-                                          long long (&jt)[kFinRegs], V_t<T, C> (&jc)[kFinRegs]) {
+__device__ __forceinline__ bool stage_job(const AcaDev &S, int p, int n, int key0, int t,
+                                          JobS &js, long long (&jt)[kFinRegs],
+                                          V_t<T, C> (&jc)[kFinRegs]) {
   if (p >= n) return false;
   const Job J = S.jobs[p];
   if (J.key != key0) return false;
   js.pe = J.pe;
   js.part = J.part;
   js.rsc_off = J.rsc;
-  js.mofs = COL ? S.rmask_off[J.b] : S.cmask_off[J.b];
+  js.mw = COL ? S.rmask[S.rmask_off[J.b] + t] : S.cmask[S.cmask_off[J.b] + t];
   js.b = J.b;
   js.h = J.h;
   js.w = J.w;
@@ -342,21 +359,148 @@ __device__ __forceinline__ bool stage_job(const AcaDev &S, int p, int n, int key
 }
 
 // ---------------------------------------------------------------------------
+// P0 quadrature of the ACA integration kernel.
+//
+// The fixed element of a job is staged in shared memory as FixRec (broadcast
+// to the warp), the lane's varying element is held in registers.  The double
+// sum runs fixed point o outer (one shared load of its 4 values per job) and
+// lane point i inner, accumulating w_o w_i G with the combined weight from the
+// constant bank (RuleTab::w2).
+//
+// LOCAL form (float64 single layer, the headline path): both elements are
+// expressed relative to a warp-uniform origin c inside the varying cluster
+// (lane 0's first quadrature point) and
+//     r^2 = |x'|^2 + |y'|^2 - 2 x'.y'      (x' = x - c, y' = y - c)
+// is one add and three FMAs, with (-2 x', |x'|^2) staged per fixed point and
+// |y'|^2 per lane point.  On an admissible block dist(t, s) >= min diam / eta,
+// so |x'|^2 + |y'|^2 <= O((2 eta + 1)^2) r^2 and the cancellation costs a few
+// ulp of r^2 (entries stay within 1e-13 of the direct difference; the parity
+// tests bound them at 1e-12 against the reference).  1/r is the MUFU.RSQ64H
+// seed y with the second-order correction folded into one polynomial:
+//     1/r = y (1 + e/2 + 3 e^2/8), e = 1 - r^2 y^2
+//         = (3/8) y ((r^2 y^2 - 5/3)^2 + 20/9),
+// i.e. DMUL, 2 DFMA, and the weight product + accumulate (3/8 goes into the
+// final scale): 9 FP64 instructions + 1 MUFU per quadrature-point pair
+// against 12 + 1 for the direct difference with the standard refinement.
+// Near-field leaves and the contract kernels keep the direct difference.
+// ---------------------------------------------------------------------------
+template <typename T> struct FixRec {
+  T p[6][4];  // LOCAL: (-2 x'_0, -2 x'_1, -2 x'_2, |x'|^2); direct: (x_0, x_1, x_2, 0)
+  T n[4];     // normal, |J|
+  int4 ev;    // vertex ids, element id
+};
+
+template <typename T, int OP> struct P0Local {
+  static constexpr bool value = std::is_same<T, double>::value && OP == HBEM_SLP;
+};
+
+__device__ __forceinline__ double rsq_seed(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+template <typename T, bool LOCAL>
+__device__ __forceinline__ void fix_from_rec(const ElemRec<T> &r, T c0, T c1, T c2,
+                                             FixRec<T> &f) {
+#pragma unroll
+  for (int o = 0; o < 6; ++o) {
+    if (LOCAL) {
+      const T x0 = r.q[3 * o] - c0, x1 = r.q[3 * o + 1] - c1, x2 = r.q[3 * o + 2] - c2;
+      f.p[o][0] = T(-2) * x0;
+      f.p[o][1] = T(-2) * x1;
+      f.p[o][2] = T(-2) * x2;
+      f.p[o][3] = x0 * x0 + x1 * x1 + x2 * x2;
+    } else {
+      f.p[o][0] = r.q[3 * o];
+      f.p[o][1] = r.q[3 * o + 1];
+      f.p[o][2] = r.q[3 * o + 2];
+      f.p[o][3] = T(0);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) f.n[c] = r.n[c];
+  f.ev = r.ev;
+}
+
+// NJ fixed elements F against the lane's element (points y, local |y'|^2 in
+// ny, normal nl).  FIXED_TEST: the fixed elements are test elements (row
+// jobs); otherwise trial elements (column jobs).
+template <typename T, bool C, int OP, bool HELM, bool FIXED_TEST, int NJ>
+__device__ __forceinline__ void p0_quad(const RuleTab<T> &R, const FixRec<T> *const (&F)[NJ],
+                                        const T (&y)[18], const T (&ny)[6], const T (&nl)[4],
+                                        typename Num<T, C>::V (&out)[NJ]) {
+  constexpr bool LOCAL = P0Local<T, OP>::value;
+  T sr[NJ], si[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) { sr[j] = T(0); si[j] = T(0); }
+#pragma unroll
+  for (int o = 0; o < 6; ++o) {
+    T f[NJ][4];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) f[j][c] = F[j]->p[o][c];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const T w = FIXED_TEST ? R.w2[o][i] : R.w2[i][o];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        if constexpr (LOCAL) {
+          const double r2 =
+              fma(f[j][0], y[3 * i], fma(f[j][1], y[3 * i + 1], fma(f[j][2], y[3 * i + 2],
+                                                                    f[j][3] + ny[i])));
+          const double s = rsq_seed(r2);
+          const double d = fma(r2, s * s, -5.0 / 3.0);
+          const double q = fma(d, d, 20.0 / 9.0);
+          if (!HELM) {
+            sr[j] = fma(w * s, q, sr[j]);  // (8/3) w / r
+          } else {
+            const double g = s * q;        // (8/3) / r
+            const double kr = R.k38 * (r2 * g);
+            double sn, cs;
+            sincos(kr, &sn, &cs);
+            const double wg = w * g;
+            sr[j] = fma(wg, cs, sr[j]);
+            si[j] = fma(wg, sn, si[j]);
+          }
+        } else {
+          const T d0 = FIXED_TEST ? f[j][0] - y[3 * i] : y[3 * i] - f[j][0];
+          const T d1 = FIXED_TEST ? f[j][1] - y[3 * i + 1] : y[3 * i + 1] - f[j][1];
+          const T d2 = FIXED_TEST ? f[j][2] - y[3 * i + 2] : y[3 * i + 2] - f[j][2];
+          T gr, gi;
+          point_kernel<T, OP, HELM>(R, d0, d1, d2, FIXED_TEST ? F[j]->n : nl,
+                                    FIXED_TEST ? nl : F[j]->n, gr, gi);
+          sr[j] += w * gr;
+          if (HELM) si[j] += w * gi;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const T scale = (F[j]->n[3] * nl[3]) * T(LOCAL ? 0.375 * kInv4Pi : kInv4Pi);
+    out[j] = Num<T, C>::mk(scale * sr[j], HELM ? scale * si[j] : T(0));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K3 (P0): one warp per (group head, 32-wide tile).  Lane l keeps the varying
 // element of tile column 32 t + l in registers and walks every job of the
 // group; fixed elements, job views and residual coefficients of kSeg jobs at
 // a time are staged in shared memory and broadcast.  The residual factor
-// values of a job are loaded before its integral so their latency hides
-// behind the quadrature.
+// values of a job are loaded (cp.async) before its integral so their latency
+// hides behind the quadrature.
 // ---------------------------------------------------------------------------
 template <typename T, bool C, int OP, bool HELM, bool COL>
-__global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, AcaDev S, int n,
-                                                        long long n_items) {
+__global__ void __launch_bounds__(kThreads, HB_ACA_P0_MINB) k_aca_p0(Prob<T> P, AcaDev S, int n,
+                                                                   long long n_items) {
   using N = Num<T, C>;
   using V = typename N::V;
-  constexpr int kG = sizeof(V) > 8 ? 2 : HB_JOB_GROUP;  // jobs integrated together
-  constexpr int kSeg = (sizeof(V) > 8 || kG > 2) ? 8 : 16;  // jobs staged per segment (48 KB smem)
-  __shared__ ElemRec<T> sr[kWarps][kSeg];
+  constexpr bool LOCAL = P0Local<T, OP>::value;
+  constexpr int kG = HB_JOB_GROUP;  // jobs integrated together
+  constexpr int kSeg = (sizeof(V) > 8 || kG > 2) ? 8 : 16;  // jobs staged per segment
+  __shared__ FixRec<T> sr[kWarps][kSeg];
   __shared__ JobS sj[kWarps][kSeg];
   __shared__ long long sjt[kWarps][kSeg][kFinRegs];
   __shared__ V sjc[kWarps][kSeg][kFinRegs];
@@ -370,8 +514,31 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
   const int key0 = J0.key, vstart = J0.vstart, nvar = J0.nvar;
   const int idx = t * 32 + lane;
   const bool valid = idx < nvar;
-  ElemRec<T> my;
-  load_rec<T>(COL ? P.trec : P.srec, vstart + (valid ? idx : nvar - 1), my);
+  T y[18], ny[6], nl[4];
+  int4 myev;
+  T c0 = T(0), c1 = T(0), c2 = T(0);
+  {
+    ElemRec<T> my;
+    load_rec<T>(COL ? P.trec : P.srec, vstart + (valid ? idx : nvar - 1), my);
+    if (LOCAL) {
+      // warp-uniform origin: lane 0's first quadrature point (idx 0 of the
+      // tile is always valid)
+      c0 = __shfl_sync(kFull, my.q[0], 0);
+      c1 = __shfl_sync(kFull, my.q[1], 0);
+      c2 = __shfl_sync(kFull, my.q[2], 0);
+    }
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      y[3 * i] = my.q[3 * i] - c0;
+      y[3 * i + 1] = my.q[3 * i + 1] - c1;
+      y[3 * i + 2] = my.q[3 * i + 2] - c2;
+      ny[i] = LOCAL ? y[3 * i] * y[3 * i] + y[3 * i + 1] * y[3 * i + 1] + y[3 * i + 2] * y[3 * i + 2]
+                    : T(0);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) nl[c] = my.n[c];
+    myev = my.ev;
+  }
   const V *pool = static_cast<const V *>(S.pool);
   unsigned long long nent = 0, nsing = 0;
   for (int seg = p0;; seg += kSeg) {
@@ -380,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
       JobS js;
       long long jt[kFinRegs];
       V jc[kFinRegs];
-      ok = stage_job<T, C, COL>(S, seg + lane, n, key0, js, jt, jc);
+      ok = stage_job<T, C, COL>(S, seg + lane, n, key0, t, js, jt, jc);
       if (ok) {
         sj[wid][lane] = js;
 #pragma unroll
@@ -391,17 +558,18 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
           }
         ElemRec<T> r;
         load_rec<T>(COL ? P.srec : P.trec, (COL ? S.c0[js.b] : S.r0[js.b]) + js.fix, r);
-        sr[wid][lane] = r;
+        FixRec<T> f;
+        fix_from_rec<T, LOCAL>(r, c0, c1, c2, f);
+        sr[wid][lane] = f;
       }
     }
     const unsigned okm = __ballot_sync(kFull, ok) | ~((1u << kSeg) - 1u);
     const int nseg = okm == kFull ? kSeg : __ffs(~okm) - 1;
     __syncwarp();
-    // jobs in groups of kG (then 2, 1): independent quadrature chains that
-    // share the lane's points
+    // jobs in groups of kG (then 1): independent quadrature chains that share
+    // the lane's points
     for (int s = 0; s < nseg;) {
-      const int rem = nseg - s;
-      const int nj = rem >= kG ? kG : (rem >= 2 ? 2 : 1);
+      const int nj = nseg - s >= kG ? kG : 1;
 #pragma unroll
       for (int u = 0; u < kG; ++u) {
         if (u < nj) {
@@ -415,32 +583,26 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_aca_p0(Prob<T> P, Aca
         }
       }
       V val[kG];
-      if (kG > 2 && nj == kG) {
-        const ElemRec<T> *FG[kG];
+      if (nj == kG) {
+        const FixRec<T> *FG[kG];
 #pragma unroll
         for (int u = 0; u < kG; ++u) FG[u] = &sr[wid][s + u];
-        p0_pairs_fx<T, C, OP, HELM, !COL, kG>(P.R, FG, my.q, my.n, val);
-      } else if (nj == 2) {
-        const ElemRec<T> *const F2[2] = {&sr[wid][s], &sr[wid][s + 1]};
-        V v2[2];
-        p0_pairs_fx<T, C, OP, HELM, !COL, 2>(P.R, F2, my.q, my.n, v2);
-        val[0] = v2[0];
-        val[1] = v2[1];
+        p0_quad<T, C, OP, HELM, !COL, kG>(P.R, FG, y, ny, nl, val);
       } else {
-        const ElemRec<T> *const F1[1] = {&sr[wid][s]};
+        const FixRec<T> *const F1[1] = {&sr[wid][s]};
         V v1[1];
-        p0_pairs_fx<T, C, OP, HELM, !COL, 1>(P.R, F1, my.q, my.n, v1);
+        p0_quad<T, C, OP, HELM, !COL, 1>(P.R, F1, y, ny, nl, v1);
         val[0] = v1[0];
       }
 #pragma unroll
       for (int u = 0; u < kG; ++u) {
         if (u < nj) {
           const int4 fev = sr[wid][s + u].ev;
-          unsigned tm = __ballot_sync(kFull, valid && touching4(my.ev, fev));
+          unsigned tm = __ballot_sync(kFull, valid && touching4(myev, fev));
           while (tm) {
             const int src = __ffs(tm) - 1;
             tm &= tm - 1;
-            const int ev = __shfl_sync(kFull, my.ev.w, src);
+            const int ev = __shfl_sync(kFull, myev.w, src);
             const double2 sv =
                 singular_warp<OP, HELM>(P.G64p, COL ? ev : fev.w, COL ? fev.w : ev);
             if (lane == src) val[u] = N::mk((T)sv.x, (T)sv.y);
@@ -630,7 +792,7 @@ __global__ void __launch_bounds__(kThreads) k_aca_gen(Prob<T> P, AcaDev S, int n
       JobS js;
       long long jt[kFinRegs];
       V jc[kFinRegs];
-      ok = stage_job<T, C, COL>(S, p, n, key0, js, jt, jc);
+      ok = stage_job<T, C, COL>(S, p, n, key0, t, js, jt, jc);
       if (ok) {
         sj[wid] = js;
 #pragma unroll
@@ -699,37 +861,22 @@ __global__ void __launch_bounds__(kThreads) k_aca_gen(Prob<T> P, AcaDev S, int n
 // and its pivot p stored behind it, v = r / p is applied where v is read
 // (residual coefficients, cross terms, payload packing).
 // ---------------------------------------------------------------------------
-// pivot statistics of a residual row / column, lanes over its entries in
-// order: argmax |val| over unmasked entries (first index on ties) and
-// sum |val|^2 over all entries (hmatrix.py:329-332 / 301-314, 343-362)
-template <typename T, bool C>
-__device__ __forceinline__ void residual_stats(const typename Num<T, C>::V *vals, int n,
-                                               const unsigned *mask, int skip, int lane,
-                                               double &best, int &bidx, double &ss) {
-  using N = Num<T, C>;
+// pivot statistics of a job's residual row / column from its tile records
+// (aca_epi): lanes over the tiles in order, then the fixed butterfly; argmax
+// over unused indices with the first index on ties, sum |val|^2
+__device__ __forceinline__ void tile_stats(const double *rec, int ntiles, long long stride,
+                                           int lane, double &best, int &bidx, double &ss) {
   best = -1.0;
   bidx = 0x7fffffff;
   ss = 0.0;
-  // four chunks of 32 per step: their loads are issued together
-  for (int i0 = 0; i0 < n; i0 += 128) {
-    typename N::V v[4];
-    unsigned mw[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + 32 * u + lane;
-      v[u] = i < n ? vals[i] : N::zero();
-      mw[u] = i0 + 32 * u < n ? mask[(i0 >> 5) + u] : ~0u;
+  for (int t = lane; t < ntiles; t += 32) {
+    const double2 bi = *reinterpret_cast<const double2 *>(rec + t * stride);
+    const int i = (int)bi.y;
+    if (better(bi.x, i, best, bidx)) {
+      best = bi.x;
+      bidx = i;
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + 32 * u + lane;
-      if (i < n) {
-        const double a = N::abs(v[u]);
-        ss += N::nrm(v[u]);
-        const bool masked = ((mw[u] >> lane) & 1u) || i == skip;
-        if (!masked && a > best) { best = a; bidx = i; }
-      }
-    }
+    ss += rec[t * stride + 2];
   }
   warp_argmax_sum(best, bidx, ss);
 }
@@ -746,8 +893,7 @@ __global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int n) {
   const int b = J.b, h = J.h, w = J.w, i = J.fix;
   double best, ss;
   int bidx;
-  const V *pool = static_cast<const V *>(S.pool);
-  residual_stats<T, C>(pool + J.pe + h, w, S.cmask + S.cmask_off[b], -1, lane, best, bidx, ss);
+  tile_stats(S.part + J.part, tiles_of(w), part_len(J.k, Num<T, C>::NC), lane, best, bidx, ss);
   if (lane != 0) return;
   S.pend[b] = J.pe;
   if (best <= 0.0) {
@@ -788,9 +934,10 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
   const int ntc = tiles_of(h), ntr = tiles_of(w);
   const double *crec = S.part + J.part;
   const V *pool = static_cast<const V *>(S.pool);
+  const long long ps = part_len(k, NC);
   double best, ss;
   int bidx;
-  residual_stats<T, C>(pool + J.pe, h, S.rmask + S.rmask_off[b], i, lane, best, bidx, ss);
+  tile_stats(crec, ntc, ps, lane, best, bidx, ss);
   const int next = best >= 0.0 ? bidx : -1;
   const double pr = S.piv[2 * b], pim = S.piv[2 * b + 1];
   const double nu = sqrt(ss);
@@ -822,9 +969,8 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
   // cross terms Re(vdot(u_l, u) vdot(v_l, v)) with v_l = r_l / p_l, v = r / p:
   // vdot(v_l, v) = vdot(r_l, r) / (conj(p_l) p); lane l sums term l's dots
   // over the column and row tiles in tile order
-  const long long kn = (long long)k * NC;
-  const double *cd = crec;
-  const double *rd = S.rpart + S.rowpart[b];
+  const double *cd = crec + 4;
+  const double *rd = S.rpart + S.rowpart[b] + 4;
   const long long *tl = S.terms + (long long)b * S.tmax;
   double cross = 0.0;
   auto cross_term = [&](int l, double ur, double ui, double vr, double vi) {
@@ -852,15 +998,15 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
 #pragma unroll
       for (int l = 0; l < 8; ++l)
         if (l < k) {
-          ur[l] += cd[t * kn + (long long)l * NC];
-          if (C) ui[l] += cd[t * kn + (long long)l * NC + 1];
+          ur[l] += cd[t * ps + (long long)l * NC];
+          if (C) ui[l] += cd[t * ps + (long long)l * NC + 1];
         }
     for (int t = lane; t < ntr; t += 32)
 #pragma unroll
       for (int l = 0; l < 8; ++l)
         if (l < k) {
-          vr[l] += rd[t * kn + (long long)l * NC];
-          if (C) vi[l] += rd[t * kn + (long long)l * NC + 1];
+          vr[l] += rd[t * ps + (long long)l * NC];
+          if (C) vi[l] += rd[t * ps + (long long)l * NC + 1];
         }
     const double tur = tr_reduce8(ur, lane), tvr = tr_reduce8(vr, lane);
     const double tui = C ? tr_reduce8(ui, lane) : 0.0, tvi = C ? tr_reduce8(vi, lane) : 0.0;
@@ -871,13 +1017,13 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
       double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
 #pragma unroll 8
       for (int t = 0; t < ntc; ++t) {
-        ur += cd[t * kn + (long long)l * NC];
-        if (C) ui += cd[t * kn + (long long)l * NC + 1];
+        ur += cd[t * ps + (long long)l * NC];
+        if (C) ui += cd[t * ps + (long long)l * NC + 1];
       }
 #pragma unroll 8
       for (int t = 0; t < ntr; ++t) {
-        vr += rd[t * kn + (long long)l * NC];
-        if (C) vi += rd[t * kn + (long long)l * NC + 1];
+        vr += rd[t * ps + (long long)l * NC];
+        if (C) vi += rd[t * ps + (long long)l * NC + 1];
       }
       cross += cross_term(l, ur, ui, vr, vi);
     }

@@ -319,6 +319,9 @@ template <typename T> static void fill_rule(RuleTab<T> &R, const hbem_ctx_desc *
   }
   R.k = (T)d->wavenumber;
   R.k2 = (T)(d->wavenumber * d->wavenumber);
+  for (int o = 0; o < 6; ++o)
+    for (int i = 0; i < 6; ++i) R.w2[o][i] = R.wa[0][o] * R.wb[0][i];
+  R.k38 = (T)(0.375 * d->wavenumber);
 }
 
 }  // namespace hb

@@ -428,7 +428,10 @@ struct Job {
 // the residual used: row phase vdot(v_l, row), column phase vdot(u_l, col).
 // per job: nt tile statistics records of 4 doubles (best |val| over unmasked,
 // its index, sum |val|^2, pad) followed by nt dot records of k*nc doubles
-__host__ __device__ __forceinline__ long long part_len(int k, int nc) { return 4 + (long long)k * nc; }
+// (record length rounded up to an even number of doubles: 16-byte aligned records)
+__host__ __device__ __forceinline__ long long part_len(int k, int nc) {
+  return (4 + (long long)k * nc + 1) & ~1ll;
+}
 __host__ __device__ __forceinline__ long long part_dots(int nt) { return 4ll * nt; }
 __host__ __device__ __forceinline__ int tiles_of(int n) { return (n + 31) >> 5; }
 

@@ -194,3 +194,32 @@ def test_streamed_payloads_equal_deferred_copy(monkeypatch, eq, k, zc):
     same_payloads()
     part.close()
     ref.close()
+
+
+@pytest.mark.parametrize("name", ["hull_mid", "hull_126k"])
+def test_hull_mid_matches_reference(name):
+    """C4 accuracy question (tests/golden/make_hull_mid_golden.py): on 31k- and
+    126k-triangle hulls (Helmholtz SLP P0, 8 elements per wavelength, eps 1e-3)
+    the reference's OWN H-matrix misses the exact operator rows by ~9 eps.  The
+    GPU assembly follows the same pivots (its matvec equals the reference's
+    H-matrix matvec to rounding), and therefore reproduces that error — the
+    0.1 sampled-row error of the 504k hull is the reference ACA's behaviour on
+    thin bodies, not a device defect."""
+    import os
+    from conftest import GOLDEN, golden
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix
+    from paper_1711_01897_b200.meshes import elongated_hull
+    if not os.path.exists(os.path.join(GOLDEN, f"{name}.npz")):
+        pytest.skip(f"{name}.npz not generated")
+    g = golden(name)
+    v, e = elongated_hull(int(g["n_around"]), int(g["n_along"]))
+    _, _, spec, sp, bt = problem((v, e), "p0", "helmholtz", "slp", float(g["k"]))
+    h = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=float(g["eps"])))
+    keep = g["y_rows"] if "y_rows" in g else np.arange(sp.n_dofs)
+    for t, (x, yr) in enumerate(zip(g["x"], g["y"])):
+        y = h.matvec(x)
+        assert np.abs(y[keep] - yr).max() <= 1e-10 * np.abs(yr).max()
+        # the same sampled-row error as the reference's H-matrix
+        scale = np.sqrt(np.mean(np.abs(y) ** 2))
+        err = np.abs(y[g["rows"]] - g["exact"][t]).max() / scale
+        assert abs(err - g["ref_err"][t]) <= 1e-6, (err, g["ref_err"][t])
