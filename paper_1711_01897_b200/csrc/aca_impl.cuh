@@ -328,6 +328,120 @@ __device__ __forceinline__ void aca_epi(const AcaDev &S, const JobS &J, const V_
   }
 }
 
+// ---------------------------------------------------------------------------
+// Branch-free epilogue of the P0 kernel, KK = min(k, kFinRegs) known at
+// compile time (dispatched once per job: in wave w nearly every job has
+// k = w, so one instantiation runs per launch).
+//
+//   residual   val -= c_l f_l for l < KK (f_l loaded here from the pool: the
+//              loads' latency is covered by the other resident warps'
+//              quadratures), then the terms beyond the register batch;
+//   pivot      argmax of |val| over unused indices with the first index on
+//              ties, exactly: the float64 bit patterns of |val| >= 0 order
+//              like the values, so two warp REDUX max (high word, then low
+//              word among the lanes holding the maximal high word) and one
+//              ballot give the winner;
+//   sums       sum |val|^2 and the KK dots vdot(f_l, val) reduced through a
+//              shared-memory transpose: G = 32 / NV lanes per value each add
+//              32 / G rows in a fixed order, then log2(G) butterfly steps.
+// ---------------------------------------------------------------------------
+template <int NV> struct TrGroup {
+  static constexpr int G = NV <= 1 ? 32 : NV <= 2 ? 16 : NV <= 4 ? 8 : NV <= 8 ? 4 : NV <= 16 ? 2 : 1;
+};
+constexpr int kRedStride = 17;  // doubles per lane row of the transpose scratch (odd: bank spread)
+
+template <int NV>
+__device__ __forceinline__ double tr_sums(const double (&v)[NV], double *red, int lane) {
+  static_assert(NV <= kRedStride, "transpose scratch too narrow");
+  constexpr int G = TrGroup<NV>::G;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) red[lane * kRedStride + i] = v[i];
+  __syncwarp();
+  const int vi = lane / G, part = lane % G;
+  double acc = 0.0;
+  if (vi < NV) {
+#pragma unroll
+    for (int r = 0; r < 32 / G; ++r) acc += red[(part + r * G) * kRedStride + vi];
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+  __syncwarp();
+  return acc;  // lanes vi * G .. vi * G + G - 1 hold value vi's sum
+}
+
+template <typename T, bool C, bool COL, int KK>
+__device__ __forceinline__ void aca_epi_p0(const AcaDev &S, const JobS &J, const V_t<T, C> *cs,
+                                           const V_t<T, C> *const *fp, V_t<T, C> *out,
+                                           double *rec, int t, int lane, bool valid,
+                                           V_t<T, C> val, double *red) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  constexpr int NC = N::NC;
+  V f[KK > 0 ? KK : 1];
+#pragma unroll
+  for (int l = 0; l < KK; ++l) f[l] = valid ? fp[l][lane] : N::zero();
+#pragma unroll
+  for (int l = 0; l < KK; ++l) val = N::fms(val, cs[l], f[l]);
+  const int k = J.k;
+  if (k > KK) {
+    // terms beyond the register batch (late waves of high-rank blocks)
+    const V *pool = static_cast<const V *>(S.pool);
+    const long long *tl = S.terms + (long long)J.b * S.tmax;
+    const int fixo = COL ? J.h + J.fix : J.fix;
+    const int ro = COL ? 0 : J.h;
+    const int idx = t * 32 + lane;
+    for (int l = KK; l < k; ++l) {
+      const long long tb = tl[l];
+      const V c = N::div(pool[tb + fixo], pool[tb + J.h + J.w]);
+      if (valid) val = N::fms(val, c, pool[tb + ro + idx]);
+    }
+  }
+  if (valid) out[lane] = val;
+  // pivot candidate of the tile
+  const bool masked = !valid || ((J.mw >> lane) & 1u) || (COL && t * 32 + lane == J.cur);
+  const unsigned long long bits =
+      masked ? 0ull : (unsigned long long)__double_as_longlong(N::abs(val));
+  const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
+  const unsigned mh = __reduce_max_sync(kFull, hi);
+  const unsigned ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+  const unsigned cand = __ballot_sync(kFull, !masked && hi == mh && lo == ml);
+  if (lane == 0) {
+    rec[0] = cand ? __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml)) : -1.0;
+    rec[1] = cand ? (double)(t * 32 + __ffs(cand) - 1) : 2147483647.0;
+  }
+  // sum |val|^2 and the register-batch dots, one transposed reduction
+  constexpr int NV = 1 + KK * NC;
+  double v[NV];
+  v[0] = valid ? N::nrm(val) : 0.0;
+#pragma unroll
+  for (int l = 0; l < KK; ++l) {
+    double dr = 0.0, di = 0.0;
+    N::cdot(dr, di, f[l], val);  // f = 0 on invalid lanes
+    v[1 + l * NC] = dr;
+    if constexpr (C) v[2 + 2 * l] = di;
+  }
+  const double sum = tr_sums<NV>(v, red, lane);
+  constexpr int G = TrGroup<NV>::G;
+  if (lane % G == 0 && lane / G < NV) rec[lane / G == 0 ? 2 : 3 + lane / G] = sum;
+  if (k > KK) {
+    const V *pool = static_cast<const V *>(S.pool);
+    const long long *tl = S.terms + (long long)J.b * S.tmax;
+    const int ro = COL ? 0 : J.h;
+    const int idx = t * 32 + lane;
+    for (int l = KK; l < k; ++l) {
+      const long long tb = tl[l];
+      double dr = 0.0, di = 0.0;
+      if (valid) N::cdot(dr, di, pool[tb + ro + idx], val);
+      dr = warp_sum_d(dr);
+      if (C) di = warp_sum_d(di);
+      if (lane == 0) {
+        rec[4 + l * NC] = dr;
+        if (C) rec[4 + l * NC + 1] = di;
+      }
+    }
+  }
+}
+
 // stage job p (lane-level) into shared memory; returns false past the group
 template <typename T, bool C, bool COL>
 __device__ __forceinline__ bool stage_job(const AcaDev &S, int p, int n, int key0, int t,
@@ -497,14 +611,17 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_P0_MINB) k_aca_p0(Prob<T> P, 
                                                                    long long n_items) {
   using N = Num<T, C>;
   using V = typename N::V;
+  constexpr int NC = N::NC;
   constexpr bool LOCAL = P0Local<T, OP>::value;
   constexpr int kG = HB_JOB_GROUP;  // jobs integrated together
   constexpr int kSeg = (sizeof(V) > 8 || kG > 2) ? 8 : 16;  // jobs staged per segment
   __shared__ FixRec<T> sr[kWarps][kSeg];
   __shared__ JobS sj[kWarps][kSeg];
-  __shared__ long long sjt[kWarps][kSeg][kFinRegs];
-  __shared__ V sjc[kWarps][kSeg][kFinRegs];
-  __shared__ V fbuf[kWarps][kG][kFinRegs * 32];
+  __shared__ const V *sfp[kWarps][kSeg][kFinRegs];  // factor values of this tile, term l
+  __shared__ V sjc[kWarps][kSeg][kFinRegs];         // residual coefficients
+  __shared__ V *sout[kWarps][kSeg];                 // this tile of the pending record
+  __shared__ double *srec[kWarps][kSeg];            // this tile's record
+  __shared__ double sred[kWarps][32 * kRedStride];  // transpose scratch
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long item = (long long)blockIdx.x * kWarps + wid;
   if (item >= n_items) return;
@@ -539,8 +656,8 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_P0_MINB) k_aca_p0(Prob<T> P, 
     for (int c = 0; c < 4; ++c) nl[c] = my.n[c];
     myev = my.ev;
   }
-  const V *pool = static_cast<const V *>(S.pool);
   unsigned long long nent = 0, nsing = 0;
+  double *red = sred[wid];
   for (int seg = p0;; seg += kSeg) {
     bool ok = false;
     if (lane < kSeg) {
@@ -550,12 +667,16 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_P0_MINB) k_aca_p0(Prob<T> P, 
       ok = stage_job<T, C, COL>(S, seg + lane, n, key0, t, js, jt, jc);
       if (ok) {
         sj[wid][lane] = js;
+        V *pool = static_cast<V *>(S.pool);
+        const int ro = COL ? 0 : js.h;
 #pragma unroll
         for (int l = 0; l < kFinRegs; ++l)
           if (l < min(js.k, kFinRegs)) {
-            sjt[wid][lane][l] = jt[l];
+            sfp[wid][lane][l] = pool + jt[l] + ro + t * 32;
             sjc[wid][lane][l] = jc[l];
           }
+        sout[wid][lane] = pool + js.pe + (COL ? 0 : js.h) + t * 32;
+        srec[wid][lane] = S.part + js.part + (long long)t * part_len(js.k, NC);
         ElemRec<T> r;
         load_rec<T>(COL ? P.srec : P.trec, (COL ? S.c0[js.b] : S.r0[js.b]) + js.fix, r);
         FixRec<T> f;
@@ -570,18 +691,6 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_P0_MINB) k_aca_p0(Prob<T> P, 
     // the lane's points
     for (int s = 0; s < nseg;) {
       const int nj = nseg - s >= kG ? kG : 1;
-#pragma unroll
-      for (int u = 0; u < kG; ++u) {
-        if (u < nj) {
-          const JobS &J = sj[wid][s + u];
-          const int kk = min(J.k, kFinRegs);
-          const int ro = COL ? 0 : J.h;
-#pragma unroll
-          for (int l = 0; l < kFinRegs; ++l)
-            if (l < kk && valid)
-              cp_async<sizeof(V)>(&fbuf[wid][u][l * 32 + lane], pool + sjt[wid][s + u][l] + ro + idx);
-        }
-      }
       V val[kG];
       if (nj == kG) {
         const FixRec<T> *FG[kG];
@@ -610,12 +719,23 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_P0_MINB) k_aca_p0(Prob<T> P, 
           }
         }
       }
-      cp_async_wait_all();
 #pragma unroll
       for (int u = 0; u < kG; ++u)
-        if (u < nj)
-          aca_epi<T, C, COL>(S, sj[wid][s + u], sjc[wid][s + u], t, lane, valid, val[u],
-                             fbuf[wid][u]);
+        if (u < nj) {
+          const int q = s + u;
+          const JobS &J = sj[wid][q];
+          const int kk = min(J.k, kFinRegs);
+#define HB_EPI(KK)                                                                           \
+  case KK:                                                                                   \
+    aca_epi_p0<T, C, COL, KK>(S, J, sjc[wid][q], sfp[wid][q], sout[wid][q], srec[wid][q], t, \
+                              lane, valid, val[u], red);                                     \
+    break;
+          switch (kk) {
+            HB_EPI(0) HB_EPI(1) HB_EPI(2) HB_EPI(3) HB_EPI(4) HB_EPI(5) HB_EPI(6) HB_EPI(7)
+            HB_EPI(8)
+          }
+#undef HB_EPI
+        }
       s += nj;
     }
     nent += valid ? nseg : 0;
