@@ -33,10 +33,7 @@ namespace hb {
 
 constexpr unsigned kFull = 0xffffffffu;
 #ifndef HB_ACA_P0_MINB
-#define HB_ACA_P0_MINB 4  // k_aca_p0 resident CTAs per SM (register cap 128)
-#endif
-#ifndef HB_JOB_GROUP
-#define HB_JOB_GROUP 1  // jobs whose quadratures run interleaved in k_aca_p0 (1 or 2)
+#define HB_ACA_P0_MINB 3  // k_aca_p0 resident CTAs per SM (register cap 168)
 #endif
 
 // ---------------------------------------------------------------------------
@@ -236,6 +233,17 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
+// read-only (non-coherent path) load of a value
+template <typename V> __device__ __forceinline__ V ld_ro(const V *p) { return __ldg(p); }
+template <> __device__ __forceinline__ Cx<double> ld_ro<Cx<double>>(const Cx<double> *p) {
+  const double2 v = __ldg(reinterpret_cast<const double2 *>(p));
+  return Cx<double>{v.x, v.y};
+}
+template <> __device__ __forceinline__ Cx<float> ld_ro<Cx<float>>(const Cx<float> *p) {
+  const float2 v = __ldg(reinterpret_cast<const float2 *>(p));
+  return Cx<float>{v.x, v.y};
+}
+
 // job view staged in shared memory by the integration kernels
 struct JobS {
   long long pe;     // pending record
@@ -358,11 +366,17 @@ __device__ __forceinline__ double tr_sums(const double (&v)[NV], double *red, in
   for (int i = 0; i < NV; ++i) red[lane * kRedStride + i] = v[i];
   __syncwarp();
   const int vi = lane / G, part = lane % G;
-  double acc = 0.0;
-  if (vi < NV) {
+  // rows part, part + G, ... added as a balanced tree (fixed order, short
+  // dependency chains)
+  constexpr int R = 32 / G;
+  double a[R];
 #pragma unroll
-    for (int r = 0; r < 32 / G; ++r) acc += red[(part + r * G) * kRedStride + vi];
-  }
+  for (int r = 0; r < R; ++r) a[r] = vi < NV ? red[(part + r * G) * kRedStride + vi] : 0.0;
+#pragma unroll
+  for (int w = 1; w < R; w *= 2)
+#pragma unroll
+    for (int r = 0; r + w < R; r += 2 * w) a[r] += a[r + w];
+  double acc = a[0];
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
   __syncwarp();
@@ -371,15 +385,12 @@ __device__ __forceinline__ double tr_sums(const double (&v)[NV], double *red, in
 
 template <typename T, bool C, bool COL, int KK>
 __device__ __forceinline__ void aca_epi_p0(const AcaDev &S, const JobS &J, const V_t<T, C> *cs,
-                                           const V_t<T, C> *const *fp, V_t<T, C> *out,
+                                           const V_t<T, C> (&f)[kFinRegs], V_t<T, C> *out,
                                            double *rec, int t, int lane, bool valid,
                                            V_t<T, C> val, double *red) {
   using N = Num<T, C>;
   using V = typename N::V;
   constexpr int NC = N::NC;
-  V f[KK > 0 ? KK : 1];
-#pragma unroll
-  for (int l = 0; l < KK; ++l) f[l] = valid ? fp[l][lane] : N::zero();
 #pragma unroll
   for (int l = 0; l < KK; ++l) val = N::fms(val, cs[l], f[l]);
   const int k = J.k;
@@ -613,8 +624,7 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_P0_MINB) k_aca_p0(Prob<T> P, 
   using V = typename N::V;
   constexpr int NC = N::NC;
   constexpr bool LOCAL = P0Local<T, OP>::value;
-  constexpr int kG = HB_JOB_GROUP;  // jobs integrated together
-  constexpr int kSeg = (sizeof(V) > 8 || kG > 2) ? 8 : 16;  // jobs staged per segment
+  constexpr int kSeg = sizeof(V) > 8 ? 8 : 16;  // jobs staged per segment
   __shared__ FixRec<T> sr[kWarps][kSeg];
   __shared__ JobS sj[kWarps][kSeg];
   __shared__ const V *sfp[kWarps][kSeg][kFinRegs];  // factor values of this tile, term l
@@ -687,56 +697,46 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_P0_MINB) k_aca_p0(Prob<T> P, 
     const unsigned okm = __ballot_sync(kFull, ok) | ~((1u << kSeg) - 1u);
     const int nseg = okm == kFull ? kSeg : __ffs(~okm) - 1;
     __syncwarp();
-    // jobs in groups of kG (then 1): independent quadrature chains that share
-    // the lane's points
-    for (int s = 0; s < nseg;) {
-      const int nj = nseg - s >= kG ? kG : 1;
-      V val[kG];
-      if (nj == kG) {
-        const FixRec<T> *FG[kG];
+    for (int q = 0; q < nseg; ++q) {
+      const JobS &J = sj[wid][q];
+      const int kk = min(J.k, kFinRegs);
+      // factor values of the residual, loaded before the quadrature so their
+      // latency hides behind it (predicated loads, no branches)
+      V f[kFinRegs];
 #pragma unroll
-        for (int u = 0; u < kG; ++u) FG[u] = &sr[wid][s + u];
-        p0_quad<T, C, OP, HELM, !COL, kG>(P.R, FG, y, ny, nl, val);
-      } else {
-        const FixRec<T> *const F1[1] = {&sr[wid][s]};
+      for (int l = 0; l < kFinRegs; ++l) {
+        const bool use = l < kk && valid;
+        const V *src = sfp[wid][q][use ? l : 0];
+        f[l] = use ? ld_ro(src + lane) : N::zero();
+      }
+      V val;
+      {
+        const FixRec<T> *const F1[1] = {&sr[wid][q]};
         V v1[1];
         p0_quad<T, C, OP, HELM, !COL, 1>(P.R, F1, y, ny, nl, v1);
-        val[0] = v1[0];
+        val = v1[0];
       }
-#pragma unroll
-      for (int u = 0; u < kG; ++u) {
-        if (u < nj) {
-          const int4 fev = sr[wid][s + u].ev;
-          unsigned tm = __ballot_sync(kFull, valid && touching4(myev, fev));
-          while (tm) {
-            const int src = __ffs(tm) - 1;
-            tm &= tm - 1;
-            const int ev = __shfl_sync(kFull, myev.w, src);
-            const double2 sv =
-                singular_warp<OP, HELM>(P.G64p, COL ? ev : fev.w, COL ? fev.w : ev);
-            if (lane == src) val[u] = N::mk((T)sv.x, (T)sv.y);
-            ++nsing;
-          }
+      {
+        const int4 fev = sr[wid][q].ev;
+        unsigned tm = __ballot_sync(kFull, valid && touching4(myev, fev));
+        while (tm) {
+          const int src = __ffs(tm) - 1;
+          tm &= tm - 1;
+          const int ev = __shfl_sync(kFull, myev.w, src);
+          const double2 sv = singular_warp<OP, HELM>(P.G64p, COL ? ev : fev.w, COL ? fev.w : ev);
+          if (lane == src) val = N::mk((T)sv.x, (T)sv.y);
+          ++nsing;
         }
       }
-#pragma unroll
-      for (int u = 0; u < kG; ++u)
-        if (u < nj) {
-          const int q = s + u;
-          const JobS &J = sj[wid][q];
-          const int kk = min(J.k, kFinRegs);
-#define HB_EPI(KK)                                                                           \
-  case KK:                                                                                   \
-    aca_epi_p0<T, C, COL, KK>(S, J, sjc[wid][q], sfp[wid][q], sout[wid][q], srec[wid][q], t, \
-                              lane, valid, val[u], red);                                     \
+#define HB_EPI(KK)                                                                             \
+  case KK:                                                                                     \
+    aca_epi_p0<T, C, COL, KK>(S, J, sjc[wid][q], f, sout[wid][q], srec[wid][q], t, lane, valid, \
+                              val, red);                                                       \
     break;
-          switch (kk) {
-            HB_EPI(0) HB_EPI(1) HB_EPI(2) HB_EPI(3) HB_EPI(4) HB_EPI(5) HB_EPI(6) HB_EPI(7)
-            HB_EPI(8)
-          }
+      switch (kk) {
+        HB_EPI(0) HB_EPI(1) HB_EPI(2) HB_EPI(3) HB_EPI(4) HB_EPI(5) HB_EPI(6) HB_EPI(7) HB_EPI(8)
+      }
 #undef HB_EPI
-        }
-      s += nj;
     }
     nent += valid ? nseg : 0;
     __syncwarp();
@@ -981,24 +981,48 @@ __global__ void __launch_bounds__(kThreads) k_aca_gen(Prob<T> P, AcaDev S, int n
 // and its pivot p stored behind it, v = r / p is applied where v is read
 // (residual coefficients, cross terms, payload packing).
 // ---------------------------------------------------------------------------
+// Finalize kernels: one 8-lane group per job (4 jobs per warp).  Jobs
+// usually span a few 32-entry tiles, so a group's lanes cover its tiles
+// (statistics) and its terms (cross-term dots) in one pass; the reductions
+// are 3-step butterflies inside the group (xor 4, 2, 1), fixed order.
+constexpr int kFinLanes = 8;
+
+__device__ __forceinline__ void group_argmax_sum(double &best, int &bidx, double &sum) {
+#pragma unroll
+  for (int o = kFinLanes / 2; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(kFull, best, o);
+    const int oi = __shfl_xor_sync(kFull, bidx, o);
+    if (better(ob, oi, best, bidx)) { best = ob; bidx = oi; }
+    sum += __shfl_xor_sync(kFull, sum, o);
+  }
+}
+
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = kFinLanes / 2; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
 // pivot statistics of a job's residual row / column from its tile records
-// (aca_epi): lanes over the tiles in order, then the fixed butterfly; argmax
+// (aca_epi): group lanes over the tiles in order, then the butterfly; argmax
 // over unused indices with the first index on ties, sum |val|^2
 __device__ __forceinline__ void tile_stats(const double *rec, int ntiles, long long stride,
-                                           int lane, double &best, int &bidx, double &ss) {
+                                           int sl, double &best, int &bidx, double &ss) {
   best = -1.0;
   bidx = 0x7fffffff;
   ss = 0.0;
-  for (int t = lane; t < ntiles; t += 32) {
-    const double2 bi = *reinterpret_cast<const double2 *>(rec + t * stride);
-    const int i = (int)bi.y;
-    if (better(bi.x, i, best, bidx)) {
-      best = bi.x;
-      bidx = i;
+  if (rec) {
+    for (int t = sl; t < ntiles; t += kFinLanes) {
+      const double2 bi = *reinterpret_cast<const double2 *>(rec + t * stride);
+      const int i = (int)bi.y;
+      if (better(bi.x, i, best, bidx)) {
+        best = bi.x;
+        bidx = i;
+      }
+      ss += rec[t * stride + 2];
     }
-    ss += rec[t * stride + 2];
   }
-  warp_argmax_sum(best, bidx, ss);
+  group_argmax_sum(best, bidx, ss);
 }
 
 // row finalize: column pivot (hmatrix.py:329-332) or vanishing row (334-338)
@@ -1006,15 +1030,17 @@ template <typename T, bool C>
 __global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int n) {
   using N = Num<T, C>;
   using V = typename N::V;
-  const int lane = threadIdx.x & 31;
-  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (p >= n) return;
-  const Job J = S.jobs[p];
-  const int b = J.b, h = J.h, w = J.w, i = J.fix;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p = gt / kFinLanes, sl = gt % kFinLanes;
+  const bool act = p < n;
+  Job J{};
+  if (act) J = S.jobs[p];
   double best, ss;
   int bidx;
-  tile_stats(S.part + J.part, tiles_of(w), part_len(J.k, Num<T, C>::NC), lane, best, bidx, ss);
-  if (lane != 0) return;
+  tile_stats(act ? S.part + J.part : nullptr, tiles_of(J.w), part_len(J.k, N::NC), sl, best,
+             bidx, ss);
+  if (!act || sl != 0) return;
+  const int b = J.b, h = J.h, w = J.w, i = J.fix;
   S.pend[b] = J.pe;
   if (best <= 0.0) {
     unsigned *rm = S.rmask + S.rmask_off[b];
@@ -1046,110 +1072,86 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
   using N = Num<T, C>;
   using V = typename N::V;
   constexpr int NC = N::NC;
-  const int lane = threadIdx.x & 31;
-  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (p >= n) return;
-  const Job J = S.jobs[p];
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p = gt / kFinLanes, sl = gt % kFinLanes;
+  const bool act = p < n;
+  Job J{};
+  if (act) J = S.jobs[p];
   const int b = J.b, h = J.h, w = J.w, j = J.fix, k = J.k, i = J.cur;
   const int ntc = tiles_of(h), ntr = tiles_of(w);
-  const double *crec = S.part + J.part;
-  const V *pool = static_cast<const V *>(S.pool);
   const long long ps = part_len(k, NC);
+  const double *crec = act ? S.part + J.part : nullptr;
   double best, ss;
   int bidx;
-  tile_stats(crec, ntc, ps, lane, best, bidx, ss);
-  const int next = best >= 0.0 ? bidx : -1;
-  const double pr = S.piv[2 * b], pim = S.piv[2 * b + 1];
-  const double nu = sqrt(ss);
-  const double nv = sqrt(S.rn2[b]) / hypot(pr, pim);
-  const double upd = nu * nv;
-  const double n2 = S.norm2[b];
-  const int kmax_b = min(S.kmax_cfg, min(h, w));
-  unsigned *rm = S.rmask + S.rmask_off[b];
-  if (n2 > 0.0 && upd <= S.eps * sqrt(n2)) {
-    if (lane == 0) {
-      S.resid[b] = upd / sqrt(n2);
-      const int sm = S.small[b] + 1;
-      S.small[b] = sm;
-      if (sm >= 2) {
-        S.status[b] = ST_CONVERGED;
-      } else {
-        set_bit(rm, i);
-        if (next < 0) {
-          S.status[b] = ST_CONVERGED;
-          S.exhausted[b] = 1;
-        } else {
-          S.cur[b] = next;
-          S.flagA[b] = 1;  // the pending record is reused
-        }
-      }
-    }
-    return;
+  tile_stats(crec, ntc, ps, sl, best, bidx, ss);
+  double n2 = 0.0, pr = 0.0, pim = 0.0, rn2 = 0.0;
+  if (act) {
+    n2 = S.norm2[b];
+    pr = S.piv[2 * b];
+    pim = S.piv[2 * b + 1];
+    rn2 = S.rn2[b];
   }
+  const int next = best >= 0.0 ? bidx : -1;
+  const double nu = sqrt(ss);
+  const double nv = sqrt(rn2) / hypot(pr, pim);
+  const double upd = nu * nv;
+  const bool small = act && n2 > 0.0 && upd <= S.eps * sqrt(n2);
   // cross terms Re(vdot(u_l, u) vdot(v_l, v)) with v_l = r_l / p_l, v = r / p:
-  // vdot(v_l, v) = vdot(r_l, r) / (conj(p_l) p); lane l sums term l's dots
-  // over the column and row tiles in tile order
-  const double *cd = crec + 4;
-  const double *rd = S.rpart + S.rowpart[b] + 4;
-  const long long *tl = S.terms + (long long)b * S.tmax;
+  // vdot(v_l, v) = vdot(r_l, r) / (conj(p_l) p); lane sl sums the dots of
+  // terms sl, sl + 8, ... over the column and row tiles in tile order
   double cross = 0.0;
-  auto cross_term = [&](int l, double ur, double ui, double vr, double vi) {
-    const V pl = pool[tl[l] + h + w];
-    const double plr = (double)N::re(pl), pli = (double)N::im(pl);
-    const double dr = plr * pr + pli * pim, di = plr * pim - pli * pr;  // conj(p_l) p
-    double qr, qi;
-    if (C) {
-      const double d = dr * dr + di * di;
-      qr = (vr * dr + vi * di) / d;
-      qi = (vi * dr - vr * di) / d;
-    } else {
-      qr = vr / dr;
-      qi = 0.0;
-    }
-    return ur * qr - ui * qi;
-  };
-  if (k <= 8) {
-    // lanes over tiles, 8 term accumulators per lane, one transposed
-    // reduction per plane (tile order within a lane, fixed tree across lanes)
-    double ur[8], ui[8], vr[8], vi[8];
-#pragma unroll
-    for (int l = 0; l < 8; ++l) { ur[l] = 0.0; ui[l] = 0.0; vr[l] = 0.0; vi[l] = 0.0; }
-    for (int t = lane; t < ntc; t += 32)
-#pragma unroll
-      for (int l = 0; l < 8; ++l)
-        if (l < k) {
-          ur[l] += cd[t * ps + (long long)l * NC];
-          if (C) ui[l] += cd[t * ps + (long long)l * NC + 1];
-        }
-    for (int t = lane; t < ntr; t += 32)
-#pragma unroll
-      for (int l = 0; l < 8; ++l)
-        if (l < k) {
-          vr[l] += rd[t * ps + (long long)l * NC];
-          if (C) vi[l] += rd[t * ps + (long long)l * NC + 1];
-        }
-    const double tur = tr_reduce8(ur, lane), tvr = tr_reduce8(vr, lane);
-    const double tui = C ? tr_reduce8(ui, lane) : 0.0, tvi = C ? tr_reduce8(vi, lane) : 0.0;
-    const int l = lane >> 2;
-    if ((lane & 3) == 0 && l < k) cross = cross_term(l, tur, tui, tvr, tvi);
-  } else {
-    for (int l = lane; l < k; l += 32) {
+  if (act && !small) {
+    const V *pool = static_cast<const V *>(S.pool);
+    const double *cd = crec + 4;
+    const double *rd = S.rpart + S.rowpart[b] + 4;
+    const long long *tl = S.terms + (long long)b * S.tmax;
+    for (int l = sl; l < k; l += kFinLanes) {
       double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
-#pragma unroll 8
       for (int t = 0; t < ntc; ++t) {
         ur += cd[t * ps + (long long)l * NC];
         if (C) ui += cd[t * ps + (long long)l * NC + 1];
       }
-#pragma unroll 8
       for (int t = 0; t < ntr; ++t) {
         vr += rd[t * ps + (long long)l * NC];
         if (C) vi += rd[t * ps + (long long)l * NC + 1];
       }
-      cross += cross_term(l, ur, ui, vr, vi);
+      const V pl = pool[tl[l] + h + w];
+      const double plr = (double)N::re(pl), pli = (double)N::im(pl);
+      const double dr = plr * pr + pli * pim, di = plr * pim - pli * pr;  // conj(p_l) p
+      double qr, qi;
+      if (C) {
+        const double d = dr * dr + di * di;
+        qr = (vr * dr + vi * di) / d;
+        qi = (vi * dr - vr * di) / d;
+      } else {
+        qr = vr / dr;
+        qi = 0.0;
+      }
+      cross += ur * qr - ui * qi;
     }
   }
-  cross = warp_sum_d(cross);
-  if (lane != 0) return;
+  cross = group_sum(cross);
+  if (!act || sl != 0) return;
+  const int kmax_b = min(S.kmax_cfg, min(h, w));
+  unsigned *rm = S.rmask + S.rmask_off[b];
+  if (small) {
+    S.resid[b] = upd / sqrt(n2);
+    const int sm = S.small[b] + 1;
+    S.small[b] = sm;
+    if (sm >= 2) {
+      S.status[b] = ST_CONVERGED;
+    } else {
+      set_bit(rm, i);
+      if (next < 0) {
+        S.status[b] = ST_CONVERGED;
+        S.exhausted[b] = 1;
+      } else {
+        S.cur[b] = next;
+        S.flagA[b] = 1;  // the pending record is reused
+      }
+    }
+    return;
+  }
   const double n2n = n2 + 2.0 * cross + upd * upd;
   S.norm2[b] = n2n;
   S.small[b] = 0;
@@ -1272,7 +1274,7 @@ int aca_phase(const Prob<T> &P, AcaDev &S, const PhaseArgs &A, int op, bool helm
     if (rc != HBEM_OK) return rc;
     if (A.int_end) HB_CUDA(cudaEventRecord(A.int_end, st));
   }
-  const unsigned fgrid = (unsigned)((n + kWarps - 1) / kWarps);
+  const unsigned fgrid = (unsigned)(((long long)n * kFinLanes + kThreads - 1) / kThreads);
   if (col) k_fin_col<T, C><<<fgrid, kThreads, 0, st>>>(S, n);
   else k_fin_row<T, C><<<fgrid, kThreads, 0, st>>>(S, n);
   HB_CUDA(cudaGetLastError());

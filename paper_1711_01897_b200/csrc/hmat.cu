@@ -1123,11 +1123,14 @@ int run_phase(hbem_hmat *H, const Prob<T> &P, int col, long long &pool_top, int 
   *n_out = n;
   if (n == 0) return HBEM_OK;
   if (!col) {
-    if (pool_top + tot.pool > S.pool_cap)
+    // kPoolSlack: the integration kernel's bulk copies of 32-entry factor
+    // tiles may read up to one 16-byte granule past the last record
+    if (pool_top + tot.pool + kPoolSlack > S.pool_cap)
       return set_error(HBEM_ERR_CAPACITY,
                        "ACA factor pool of %lld values exhausted at wave %d (need %lld more)",
-                       (long long)S.pool_cap, wave, (long long)(pool_top + tot.pool - S.pool_cap));
-    HB_CHECK(H->vpool.grow((size_t)(pool_top + tot.pool) * H->vbytes));
+                       (long long)S.pool_cap, wave,
+                       (long long)(pool_top + tot.pool + kPoolSlack - S.pool_cap));
+    HB_CHECK(H->vpool.grow((size_t)(pool_top + tot.pool + kPoolSlack) * H->vbytes));
     S.pool_base = pool_top;
     pool_top += tot.pool;
   }

@@ -5,7 +5,7 @@
 # Select one at run time with HBEM_LIB=var/lib_G1_M4.so.
 set -e
 cd "$(dirname "$0")/../.."
-make -s all
+make -s -j8 all
 mkdir -p var build/var
 OTHER=$(ls build/*.o | grep -v kern_f64.o | grep -v kern_f32.o)
 for v in $1; do
