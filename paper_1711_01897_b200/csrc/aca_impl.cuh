@@ -32,6 +32,7 @@
 namespace hb {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kNeedThreads = 256;  // k_need block size (block-scan width)
 #ifndef HB_ACA_P0_MINB
 #define HB_ACA_P0_MINB 3  // k_aca_p0 resident CTAs per SM (register cap 168)
 #endif
@@ -72,12 +73,12 @@ static __global__ void k_phase_flags(const unsigned char *flag, const int *order
 }
 
 template <int NC>
-__global__ void k_need(AcaDev S, int na, int col, int NT_, int NS_) {
+__global__ void __launch_bounds__(kNeedThreads) k_need(AcaDev S, int na, int col, int NT_, int NS_,
+                                                      Need *bsum) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= na) return;
   const int n = *S.nlist;
   Need d{0, 0, 0, 0, 0};
-  if (p < n) {
+  if (p < n && p < na) {
     const int b = S.list[p];
     const int h = S.h[b], w = S.w[b], k = S.rank[b];
     const int tiles = tiles_of(col ? h : w);
@@ -99,7 +100,37 @@ __global__ void k_need(AcaDev S, int na, int col, int NT_, int NS_) {
       d.rsc = ne * (col ? NT_ : NS_);
     }
   }
-  S.need[p] = d;
+  // block-local inclusive scan; k_need_carry adds the preceding blocks' totals
+  using BS = cub::BlockScan<Need, kNeedThreads>;
+  __shared__ typename BS::TempStorage ts;
+  Need inc;
+  BS(ts).InclusiveScan(d, inc, SumNeed());
+  if (p < na) {
+    S.need[p] = d;
+    S.scan[p] = inc;
+  }
+  if (threadIdx.x == kNeedThreads - 1) bsum[blockIdx.x] = inc;
+}
+
+// exclusive scan of the block totals, one CTA (in place)
+static __global__ void __launch_bounds__(1024) k_need_blocks(Need *bsum, int nb) {
+  using BS = cub::BlockScan<Need, 1024>;
+  __shared__ typename BS::TempStorage ts;
+  Need carry{0, 0, 0, 0, 0};
+  for (int base = 0; base < nb; base += 1024) {
+    const int i = base + threadIdx.x;
+    Need v = i < nb ? bsum[i] : Need{0, 0, 0, 0, 0};
+    Need ex, tot;
+    BS(ts).ExclusiveScan(v, ex, Need{0, 0, 0, 0, 0}, SumNeed(), tot);
+    __syncthreads();
+    if (i < nb) bsum[i] = SumNeed()(carry, ex);
+    carry = SumNeed()(carry, tot);
+  }
+}
+
+static __global__ void k_need_carry(AcaDev S, int na, const Need *bsum) {
+  const int p = (blockIdx.x + 1) * kNeedThreads + threadIdx.x;
+  if (p < na) S.scan[p] = SumNeed()(bsum[blockIdx.x + 1], S.scan[p]);
 }
 
 template <typename T, bool C>
@@ -1037,8 +1068,22 @@ __global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int n) {
   if (act) J = S.jobs[p];
   double best, ss;
   int bidx;
-  tile_stats(act ? S.part + J.part : nullptr, tiles_of(J.w), part_len(J.k, N::NC), sl, best,
-             bidx, ss);
+  const long long ps = part_len(J.k, N::NC);
+  tile_stats(act ? S.part + J.part : nullptr, tiles_of(J.w), ps, sl, best, bidx, ss);
+  if (act && sl < min(J.k, kFinRegs)) {
+    // this row's dots with the first terms, summed over its tiles in order,
+    // for the column finalize's cross terms (compact, indexed by block)
+    const double *rd = S.part + J.part + 4 + sl * N::NC;
+    const int ntr = tiles_of(J.w);
+    double sr = 0.0, si = 0.0;
+    for (int t = 0; t < ntr; ++t) {
+      sr += rd[t * ps];
+      if (C) si += rd[t * ps + 1];
+    }
+    double *o = S.rsum + (long long)J.b * (kFinRegs * 2) + sl * 2;
+    o[0] = sr;
+    o[1] = si;
+  }
   if (!act || sl != 0) return;
   const int b = J.b, h = J.h, w = J.w, i = J.fix;
   S.pend[b] = J.pe;
@@ -1111,9 +1156,15 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
         ur += cd[t * ps + (long long)l * NC];
         if (C) ui += cd[t * ps + (long long)l * NC + 1];
       }
-      for (int t = 0; t < ntr; ++t) {
-        vr += rd[t * ps + (long long)l * NC];
-        if (C) vi += rd[t * ps + (long long)l * NC + 1];
+      if (l < kFinRegs) {
+        const double *o = S.rsum + (long long)b * (kFinRegs * 2) + l * 2;
+        vr = o[0];
+        vi = o[1];
+      } else {
+        for (int t = 0; t < ntr; ++t) {
+          vr += rd[t * ps + (long long)l * NC];
+          if (C) vi += rd[t * ps + (long long)l * NC + 1];
+        }
       }
       const V pl = pool[tl[l] + h + w];
       const double plr = (double)N::re(pl), pli = (double)N::im(pl);
@@ -1207,10 +1258,16 @@ int aca_select(const Prob<T> &, AcaDev &S, const PhaseArgs &A, cudaStream_t st) 
     HB_CUDA(cudaMemsetAsync(S.flagA, 0, na, st));
     HB_CUDA(cudaMemsetAsync(S.flagC, 0, na, st));
   }
-  k_need<NC><<<(na + 255) / 256, 256, 0, st>>>(S, na, A.col_phase, A.nt, A.ns);
+  // inclusive scan of the needs: block scans + one CTA over the block totals +
+  // carry add (three light kernels instead of a generic 40-byte-record scan)
+  const int nb = (na + kNeedThreads - 1) / kNeedThreads;
+  Need *bsum = reinterpret_cast<Need *>(A.cub_tmp);
+  k_need<NC><<<nb, kNeedThreads, 0, st>>>(S, na, A.col_phase, A.nt, A.ns, bsum);
   HB_CUDA(cudaGetLastError());
-  tb = A.cub_bytes;
-  HB_CUDA(cub::DeviceScan::InclusiveScan(A.cub_tmp, tb, S.need, S.scan, SumNeed(), na, st));
+  k_need_blocks<<<1, 1024, 0, st>>>(bsum, nb);
+  HB_CUDA(cudaGetLastError());
+  if (nb > 1) k_need_carry<<<nb - 1, kNeedThreads, 0, st>>>(S, na, bsum);
+  HB_CUDA(cudaGetLastError());
   return HBEM_OK;
 }
 
@@ -1218,8 +1275,7 @@ inline size_t aca_cub_bytes_impl(int na) {
   size_t b1 = 0, b2 = 0;
   cub::DeviceSelect::Flagged(nullptr, b1, (const int *)nullptr, (const unsigned char *)nullptr,
                              (int *)nullptr, (int *)nullptr, std::max(na, 1));
-  cub::DeviceScan::InclusiveScan(nullptr, b2, (const Need *)nullptr, (Need *)nullptr, SumNeed(),
-                                 std::max(na, 1));
+  b2 = ((size_t)std::max(na, 1) + kNeedThreads - 1) / kNeedThreads * sizeof(Need) + 256;
   return std::max(b1, b2);
 }
 

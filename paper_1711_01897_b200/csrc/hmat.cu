@@ -889,6 +889,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   HB_CHECK(dalloc(H, &S.piv, 2 * (size_t)na));
   HB_CHECK(dalloc(H, &S.pend, na));
   HB_CHECK(dalloc(H, &S.rowpart, na));
+  HB_CHECK(dalloc(H, &S.rsum, (size_t)na * kFinRegs * 2));
   HB_CHECK(dalloc(H, &S.terms, (size_t)na * S.tmax));
   HB_CHECK(dalloc(H, &S.rmask, rmw));
   HB_CHECK(dalloc(H, &S.cmask, cmw));

@@ -457,6 +457,8 @@ struct AcaDev {
   double *norm2, *resid, *rn2, *piv;  // piv: pivot of the pending row (re, im)
   long long *pend, *terms;            // pending record, accepted term records (tmax per block)
   long long *rowpart;                 // row-phase partial record 0 of the block's pending row
+  double *rsum;                       // row-phase dots of the first kFinRegs terms summed over
+                                      // the tiles (kFinRegs x 2 per block, k_fin_row)
   int tmax;
   unsigned *rmask, *cmask;
   const long long *rmask_off, *cmask_off;
