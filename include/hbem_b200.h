@@ -219,6 +219,8 @@ typedef struct hbem_hmat_stats {
   double seconds_finalize;   /* payload classification + dense expansion */
   double int_kernel_ms;      /* CUDA-event time of the ACA integration launches (k_aca_*) */
   int64_t int_launches;      /* number of those launches */
+  int64_t sing_table_pairs;  /* touching element pairs Sauter-Schwab-integrated per execute
+                                (the near-field leaves of this handle only) */
 } hbem_hmat_stats;
 
 /* setup (partition upload, state allocation) + one execute */

@@ -99,7 +99,8 @@ class HmatStats(C.Structure):
         "launches", "aca_entries")] + [
         (n, C.c_double) for n in ("aca_kernel_ms", "nearfield_kernel_ms", "seconds",
                                   "seconds_setup", "seconds_aca", "seconds_finalize")] + [
-        ("int_kernel_ms", C.c_double), ("int_launches", C.c_int64)]
+        ("int_kernel_ms", C.c_double), ("int_launches", C.c_int64),
+        ("sing_table_pairs", C.c_int64)]
 
 
 # (name, restype, argtypes) of every exported symbol in include/hbem_b200.h

@@ -78,11 +78,16 @@ def assemble_dense(spec, test_space, trial_space, config: AssemblyConfig,
         raise CapacityError(f"dense {n_rows} x {n_cols} matrix needs {need:,} bytes, "
                             f"config allows {config.max_matrix_bytes:,}")
     tree = cluster_trees_for(test_space, trial_space, eta=0.0)
+    # eta = 0 still admits clusters of zero diameter (coincident DOF centres,
+    # e.g. P1d at a vertex): every leaf is forced dense so the sweep is exact
+    tree.leaf_array[:, 2] = 0
     hstats: dict = {}
     h = assemble_hmatrix(spec, test_space, trial_space, tree, AcaConfig(), use,
                          HConfig(regular_order=config.regular_order,
                                  singular_base_order=config.singular_base_order),
                          stats=hstats)
+    if int(hstats.get("lowrank_leaves", 0)) != 0:
+        raise AssemblyError("dense assembly produced low-rank leaves")
     A = h.to_dense()
     if stats is not None:
         m = len(test_space.mesh.elements)

@@ -513,6 +513,7 @@ struct hbem_hmat {
   std::vector<long long> ad_off, ad_rowbase;
   long long nf_rows = 0;
   const long long *nf_rowbase = nullptr;
+  long long sing_pairs_table = 0;  // Sauter-Schwab pairs of this handle's table
   bool mv_dirty = true;
   void *mv_buf = nullptr;  // x, y, xt, yt
   int *mv_ad = nullptr;
@@ -850,8 +851,10 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
     H->eitems_cap = std::max<long long>(et, 1);
   }
   AcaDev &S = H->S;
-  int tmax = d->rank_capacity > 0 ? d->rank_capacity : 64;
-  S.tmax = std::min(tmax, 256);
+  if (d->rank_capacity > (1 << 16))
+    return set_error(HBEM_ERR_CONFIG, "rank_capacity %lld exceeds %d",
+                     (long long)d->rank_capacity, 1 << 16);
+  S.tmax = d->rank_capacity > 0 ? (int)d->rank_capacity : 64;
   S.kmax_cfg = d->k_max > 0 ? (int)std::min<int64_t>(d->k_max, 1 << 30) : (1 << 30);
   S.eps = d->epsilon;
   {
@@ -958,6 +961,18 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
       const bool sym = (ctx->op == HBEM_SLP || ctx->op == HBEM_HYPS) && nt == ns &&
                        ctx->test_family == ctx->trial_family;
       HB_CHECK(build_sing_table(ctx->elem, (int)m, (int)ctx->nv, sym, tab, H->dev_allocs, 0));
+      if (H->p0) {
+        // only the touching pairs of this handle's near-field leaves (the
+        // admissible leaves' rare touching pairs are integrated in place by
+        // k_aca_p0): a multi-GPU split shards the singular work too
+        std::vector<int> cinv((size_t)m, -1);
+        for (int64_t i = 0; i < d->n_cols; ++i) cinv[(size_t)d->col_perm[i]] = (int)i;
+        int *dci;
+        HB_CHECK(upload(H, &dci, cinv));
+        HB_CHECK(restrict_sing_pairs(tab, H->rperm, dci, H->nf_rowbase, nd, H->nf_rows, D.r0,
+                                     D.c0, D.w, H->dev_allocs, 0));
+      }
+      H->sing_pairs_table = tab.n_pairs;
       D.nb_ptr = tab.nb_ptr;
       D.nb_idx = tab.nb_idx;
       D.spairs = tab.pairs;
@@ -1602,6 +1617,7 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   ST.seconds_aca = secs(t0, t_aca);
   ST.seconds_finalize = secs(t_aca, t_end);
   ST.launches = launches;
+  ST.sing_table_pairs = H->sing_pairs_table;
   return HBEM_OK;
 }
 

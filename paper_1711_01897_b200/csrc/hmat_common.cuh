@@ -518,6 +518,14 @@ struct SingTable {
 };
 int build_sing_table(const int4 *d_elem, int m, int nv, bool symmetric, SingTable &out,
                      std::vector<void *> &allocs, cudaStream_t st);
+// keep only the touching pairs some near-field leaf of this handle reads
+// (P0: row element in the leaf's row cluster, trial element in its column
+// cluster), so a rank assembling a slice of the leaves integrates only its
+// share of the Sauter-Schwab table
+int restrict_sing_pairs(SingTable &tab, const int *rperm, const int *cinv,
+                        const long long *rowbase, int nd, long long nrows, const int *r0,
+                        const int *c0, const int *w, std::vector<void *> &allocs,
+                        cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // launchers (aca_f64.cu / aca_f32.cu, near_f64.cu / near_f32.cu)

@@ -135,8 +135,9 @@ template <typename T, bool C>
 int sing_table_launch(const Prob<T> &P, const DenseDev &D, int op, bool helm, int nt, int ns,
                       cudaStream_t st) {
   if (D.n_spairs <= 0) return HBEM_OK;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);  // the context's device (set by the caller)
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned grid =
       (unsigned)std::min<long long>((D.n_spairs + kWarps - 1) / kWarps, (long long)sms * 16);
   return dispatch_op(op, helm, nt, ns, [&](auto OPc, auto Hc, auto NTc, auto NSc) -> int {

@@ -140,7 +140,73 @@ int scan_counts(const int *cnt, int *ptr, int n, cudaStream_t st, long long *tot
   return HBEM_OK;
 }
 
+// one thread per near-field leaf row: mark the neighbour slots (e, f) whose
+// trial element f lies in the leaf's column cluster
+__global__ void k_mark_rows(const int *nb_ptr, const int *nb_idx, const int *rperm,
+                            const int *cinv, const long long *rowbase, int nd, long long nrows,
+                            const int *r0, const int *c0, const int *w, unsigned char *mark) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g >= nrows) return;
+  int lo = 0, hi = nd;  // leaf s with rowbase[s] <= g < rowbase[s + 1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (rowbase[mid] <= g) lo = mid;
+    else hi = mid;
+  }
+  const int s = lo;
+  const int e = rperm[r0[s] + (int)(g - rowbase[s])];
+  const int cb = c0[s], ce = c0[s] + w[s];
+  for (int j = nb_ptr[e]; j < nb_ptr[e + 1]; ++j) {
+    const int tp = cinv[nb_idx[j]];
+    if (tp >= cb && tp < ce) mark[j] = 1;
+  }
+}
+
+__global__ void k_pair_flags(const int4 *pairs, long long np, const unsigned char *mark,
+                             unsigned char *flag) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= np) return;
+  const int4 p = pairs[q];
+  flag[q] = mark[p.z] || (p.w >= 0 && mark[p.w]);
+}
+
 }  // namespace
+
+int restrict_sing_pairs(SingTable &tab, const int *rperm, const int *cinv,
+                        const long long *rowbase, int nd, long long nrows, const int *r0,
+                        const int *c0, const int *w, std::vector<void *> &allocs,
+                        cudaStream_t st) {
+  if (tab.n_pairs <= 0) return HBEM_OK;
+  unsigned char *mark = nullptr, *flag = nullptr;
+  int *cnt = nullptr;
+  HB_CUDA(cudaMalloc(&mark, (size_t)std::max<long long>(tab.nnz, 1)));
+  HB_CUDA(cudaMalloc(&flag, (size_t)tab.n_pairs));
+  HB_CUDA(cudaMalloc(&cnt, 4));
+  HB_CUDA(cudaMemsetAsync(mark, 0, (size_t)std::max<long long>(tab.nnz, 1), st));
+  if (nrows > 0)
+    k_mark_rows<<<(unsigned)((nrows + 255) / 256), 256, 0, st>>>(
+        tab.nb_ptr, tab.nb_idx, rperm, cinv, rowbase, nd, nrows, r0, c0, w, mark);
+  k_pair_flags<<<(unsigned)((tab.n_pairs + 255) / 256), 256, 0, st>>>(tab.pairs, tab.n_pairs,
+                                                                      mark, flag);
+  int4 *kept = nullptr;
+  HB_CHECK(alloc(allocs, &kept, (size_t)tab.n_pairs));
+  size_t tb = 0;
+  HB_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, tab.pairs, flag, kept, cnt, tab.n_pairs, st));
+  void *tmp = nullptr;
+  HB_CUDA(cudaMalloc(&tmp, std::max<size_t>(tb, 1)));
+  cudaError_t e = cub::DeviceSelect::Flagged(tmp, tb, tab.pairs, flag, kept, cnt, tab.n_pairs, st);
+  int h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, cnt, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(tmp);
+  cudaFree(mark);
+  cudaFree(flag);
+  cudaFree(cnt);
+  HB_CUDA(e);
+  tab.pairs = kept;
+  tab.n_pairs = h;
+  return HBEM_OK;
+}
 
 int build_sing_table(const int4 *d_elem, int m, int nv, bool symmetric, SingTable &out,
                      std::vector<void *> &allocs, cudaStream_t st) {

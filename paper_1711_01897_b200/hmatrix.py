@@ -197,6 +197,7 @@ class _DevicePart:
         st = _lib.HmatStats()
         check(lib.hbem_hmat_stats_get(handle, C.byref(st)))
         self.stats = {name: getattr(st, name) for name, _ in _lib.HmatStats._fields_}
+        self.stats["capacity_retries"] = getattr(self, "capacity_retries", 0)
         self._arenas = None
 
     def execute(self, stream=None):
@@ -358,14 +359,28 @@ def compression_stats(h: HMatrix) -> CompressionStats:
                             n_low)
 
 
+# Sauter-Schwab work per touching pair in regular-pair units: a P0 element
+# touches ~13 elements (itself, 3 across edges, ~9 across vertices) with
+# 1536 / 1280 / 512 points against 36, and the single layer integrates each
+# unordered pair once: ~ (1536 + 3 * 1280 + 9 * 512) / 36 / 2 per element
+_SING_PER_DIAG_ROW = 140.0
+_SING_PER_OFFDIAG = 20.0
+
+
 def _leaf_costs(tree: BlockClusterTree, k_est: float = 8.0) -> np.ndarray:
-    """Cost model for the multi-GPU split: admissible leaves
-    ~ (k_est + 2) (h + w) pair integrals, near-field h w."""
+    """Cost model for the multi-GPU split, in regular element-pair
+    integrals: admissible leaves ~ (k_est + 2) (h + w) (rank + confirmation
+    rows and columns); near-field leaves h w plus their Sauter-Schwab pairs,
+    which each rank integrates only for its own leaves (diagonal leaves hold
+    every element's touching neighbours, off-diagonal neighbours only the
+    ones along the shared boundary, ~ sqrt(h w))."""
     la = tree.leaf_array
     rn, cn = tree.rows.node_array, tree.cols.node_array
     h = (rn[la[:, 0], 1] - rn[la[:, 0], 0]).astype(np.float64)
     w = (cn[la[:, 1], 1] - cn[la[:, 1], 0]).astype(np.float64)
-    return np.where(la[:, 2] == 1, (k_est + 2.0) * (h + w), h * w)
+    diag = la[:, 0] == la[:, 1] if tree.rows is tree.cols else np.zeros(len(la), bool)
+    sing = np.where(diag, _SING_PER_DIAG_ROW * h, _SING_PER_OFFDIAG * np.sqrt(h * w))
+    return np.where(la[:, 2] == 1, (k_est + 2.0) * (h + w), h * w + sing)
 
 
 def split_leaves(tree: BlockClusterTree, parts: int) -> list[np.ndarray]:
@@ -419,13 +434,32 @@ def _assemble_part(dev_ctx, tree: BlockClusterTree, leaf_ids, test_space, trial_
         d.out_u, d.out_v, d.out_dense = (_lib.vptr(a) for a in out)
         d.out_u_cap, d.out_v_cap, d.out_dense_cap = (len(a) for a in out)
     h = C.c_void_p()
-    check(lib.hbem_hmat_assemble(dev_ctx.handle, C.byref(d), stream, C.byref(h)))
+    # rank capacity (the per-block factor-table size of the device ACA): the
+    # reference's ACA runs on to min(m, n) terms, so a block that exhausts the
+    # table re-runs the assembly with a doubled table (up to the largest
+    # admissible block dimension, where the k_max fallback always applies
+    # first) instead of failing
+    cap, retries = int(acfg.rank_capacity), 0
+    rsz, csz = rn[:, 1] - rn[:, 0], cn[:, 1] - cn[:, 0]
+    adm = la[:, 2] == 1
+    kcap = int(np.minimum(rsz[la[adm, 0]], csz[la[adm, 1]]).max()) if adm.any() else 1
+    while True:
+        d.rank_capacity = cap
+        status = lib.hbem_hmat_assemble(dev_ctx.handle, C.byref(d), stream, C.byref(h))
+        if status == _lib.HBEM_OK:
+            break
+        msg = lib.hbem_last_error().decode("utf-8", "replace")
+        if status != 2 or "rank capacity" not in msg or cap >= kcap:
+            check(status)
+        cap, retries = min(2 * cap, max(kcap, 1)), retries + 1
     def shapes():  # leaf (h, w), only needed for host payload views
         rsz, csz = rn[:, 1] - rn[:, 0], cn[:, 1] - cn[:, 0]
         return np.stack([rsz[la[:, 0]], csz[la[:, 1]]], 1)
 
     part = _DevicePart(h, len(la), shapes, dev_ctx.spec.result_dtype, n_rows=len(rp),
                        context=dev_ctx)
+    part.capacity_retries = retries
+    part.stats["capacity_retries"] = retries
     if out is not None:
         s = part.stats
         part._arenas = (out[0][: s["u_entries"]], out[1][: s["v_entries"]],
@@ -495,7 +529,7 @@ def assemble_hmatrix(spec: OperatorSpec, test_space, trial_space, block_tree: Bl
                 agg[key] += int(s[key])
             agg["backend_jobs"] += int(s["row_jobs"] + s["col_jobs"])
             for key in ("regular_pairs", "waves", "row_jobs", "col_jobs", "u_entries",
-                        "v_entries", "dense_entries"):
+                        "v_entries", "dense_entries", "capacity_retries", "sing_table_pairs"):
                 extra[key] = extra.get(key, 0) + int(s[key])
             extra["device_seconds"] = max(extra.get("device_seconds", 0.0), float(s["seconds"]))
         stats.update(agg)

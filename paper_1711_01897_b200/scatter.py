@@ -346,16 +346,20 @@ def burton_miller_solve(cfg: ScatterConfig, wave: PlaneWave | None = None, mode:
     if mode == "dense":
         from .assembly import assemble_dense
         n_dev = cfg.assembly.devices or 1
+        orders = dict(regular_order=cfg.assembly.regular_order,
+                      singular_base_order=cfg.assembly.singular_base_order)
         k_op = assemble_dense(spec_k, p1c, p1c, cfg.assembly,
-                              make_gpu_backends(make_integration_context(spec_k, p1c, p1c), n_dev))
+                              make_gpu_backends(make_integration_context(spec_k, p1c, p1c,
+                                                                         **orders), n_dev))
         s_op = assemble_dense(spec_s, p1d, p1d, cfg.assembly,
-                              make_gpu_backends(make_integration_context(spec_s, p1d, p1d), n_dev))
+                              make_gpu_backends(make_integration_context(spec_s, p1d, p1d,
+                                                                         **orders), n_dev))
         apply_k, apply_s = k_op.__matmul__, s_op.__matmul__
     else:
         k_op = assemble_hmatrix(spec_k, p1c, p1c, cluster_trees_for(p1c, p1c, cfg.n_min, cfg.eta),
-                                cfg.aca)
+                                cfg.aca, assembly_config=cfg.assembly)
         s_op = assemble_hmatrix(spec_s, p1d, p1d, cluster_trees_for(p1d, p1d, cfg.n_min, cfg.eta),
-                                cfg.aca)
+                                cfg.aca, assembly_config=cfg.assembly)
         apply_k, apply_s = k_op.matvec, s_op.matvec
     eta_c = 1.0 / (1j * k)
 

@@ -64,3 +64,23 @@ def test_dense_p1c_dlp_equals_oracle_and_capacity_error():
     assert np.abs(A - ref).max() <= 1e-12 * np.abs(ref).max()
     with pytest.raises(CapacityError, match="bytes"):
         assemble_dense(spec, sp, sp, AssemblyConfig(max_matrix_bytes=8), be)
+
+
+@pytest.mark.gpu
+def test_dense_p1d_hull_with_poles_is_exact():
+    """eta = 0 admits zero-diameter clusters (the hull's 40-valent poles give
+    40 coincident P1d DOF centres, 126 such leaves); the dense sweep forces
+    them dense, so the matrix is the exact Galerkin one."""
+    from oracle import hbem_oracle as O
+    from paper_1711_01897_b200.assembly import AssemblyConfig, assemble_dense
+    from paper_1711_01897_b200.backend import make_gpu_backends
+    from paper_1711_01897_b200.discretization import (OperatorSpec, TriangleMesh, build_space,
+                                                      make_integration_context)
+    from paper_1711_01897_b200.meshes import elongated_hull
+    v, e = elongated_hull(40, 6)
+    sp = build_space(TriangleMesh(v, e), "p1d")
+    spec = OperatorSpec("helmholtz", "slp", 3.0)
+    A = assemble_dense(spec, sp, sp, AssemblyConfig(),
+                       make_gpu_backends(make_integration_context(spec, sp, sp)))
+    ref = O.assemble_dense(O.Problem(O.Spec("helmholtz", "slp", 3.0), v, e, "p1d", "p1d"))
+    assert np.abs(A - ref).max() <= 1e-12 * np.abs(ref).max()

@@ -191,3 +191,27 @@ def test_api_errors():
     wrong = make_gpu_backends(make_integration_context(other, sp1, sp1))
     with pytest.raises(ConfigError, match="different operator spec"):
         assemble_hmatrix(spec, sp1, sp1, bt1, AcaConfig(), wrong)
+
+
+def test_rank_capacity_overflow_retries_with_larger_table():
+    """A factor table smaller than the ranks ACA reaches (rank_capacity 2 at
+    eps 1e-8) re-runs the assembly with a doubled table instead of failing
+    (the reference's aca runs on to min(m, n)); the payloads equal those of a
+    run with ample capacity."""
+    from paper_1711_01897_b200.discretization import OperatorSpec, TriangleMesh, build_space
+    from paper_1711_01897_b200.hmatrix import (AcaConfig, AssemblyConfig, assemble_hmatrix,
+                                               hmat_matvec)
+    from paper_1711_01897_b200.meshes import geodesic_sphere
+    from paper_1711_01897_b200.partition import cluster_trees_for
+    v, e = geodesic_sphere(12)
+    sp = build_space(TriangleMesh(v, e), "p0")
+    bt = cluster_trees_for(sp, sp)
+    spec = OperatorSpec("laplace", "slp", 0.0)
+    st_small, st_big = {}, {}
+    h1 = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=1e-8), None,
+                          AssemblyConfig(rank_capacity=2), stats=st_small)
+    h2 = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=1e-8), None,
+                          AssemblyConfig(rank_capacity=256), stats=st_big)
+    assert st_small["capacity_retries"] >= 2 and st_big["capacity_retries"] == 0
+    x = np.random.default_rng(5).standard_normal(sp.n_dofs)
+    assert np.array_equal(hmat_matvec(h1, x, device=False), hmat_matvec(h2, x, device=False))
