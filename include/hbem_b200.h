@@ -238,6 +238,11 @@ int hbem_hmat_leaf_meta(const hbem_hmat *h, int32_t *kind, int32_t *rank, int32_
 int hbem_hmat_copy_arenas(const hbem_hmat *h, void *u, void *v, void *dense);
 /* y = H x in original DOF order; x, y host arrays of the result dtype. */
 int hbem_hmat_matvec(const hbem_hmat *h, const void *x, void *y);
+/* y = H x with x (n_cols) and y (n_rows) DEVICE pointers in the original DOF
+ * order, enqueued on `stream` (no host synchronisation); bit-reproducible:
+ * every leaf contribution lands in its own slot and rows add them in the
+ * reference's fixed (row start, column start) leaf order (hmatrix.py:441-470) */
+int hbem_hmat_matvec_device(const hbem_hmat *h, const void *d_x, void *d_y, void *stream);
 int hbem_hmat_destroy(hbem_hmat *h);
 
 /* Far-field potential of a surface density, evaluate_far_field

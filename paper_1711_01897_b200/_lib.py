@@ -142,6 +142,7 @@ SIGNATURES = [
      [C.c_void_p, c_int32_p, c_int32_p, c_int32_p, c_int64_p, c_int64_p, c_int64_p]),
     ("hbem_hmat_copy_arenas", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("hbem_hmat_matvec", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("hbem_hmat_matvec_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("hbem_hmat_destroy", C.c_int, [C.c_void_p]),
     ("hbem_host_alloc", C.c_int, [C.c_int64, C.POINTER(C.c_void_p)]),
     ("hbem_host_free", C.c_int, [C.c_void_p]),

@@ -522,6 +522,16 @@ struct hbem_hmat {
   long long *mv_sbase = nullptr;  // per low-rank list position
   void *mv_s = nullptr;
   long long mv_nd = 0, mv_nr = 0, mv_ns = 0;
+  // deterministic matvec: partial slots, chunk dots, cover lists (device)
+  void *mv_part = nullptr, *mv_dpart = nullptr;
+  long long *mv_ifirst = nullptr, *mv_ibase = nullptr, *mv_rbase = nullptr;
+  int *mv_cstart = nullptr;
+  long long *mv_cptr = nullptr, *mv_cover = nullptr;
+  int mv_ncl = 0;
+  long long mv_ad_rows = 0;
+  // host copies for the matvec's cover lists
+  std::vector<int> nf_r0, nf_c0, nf_h;
+  std::vector<int> rleaf_start;  // row clusters of the tree's leaves (sorted starts + n_rows)
   // streamed payloads: per-wave packing of converged low-rank blocks into
   // device U / V arenas (growable), optional D2H into caller host arenas
   VPool uarena, varena;
@@ -566,6 +576,9 @@ struct hbem_hmat {
     cudaFree(mv_items);
     cudaFree(mv_sbase);
     cudaFree(mv_s);
+    cudaFree(mv_part); cudaFree(mv_dpart);
+    cudaFree(mv_ifirst); cudaFree(mv_ibase); cudaFree(mv_rbase);
+    cudaFree(mv_cstart); cudaFree(mv_cptr); cudaFree(mv_cover);
     if (mail) cudaFreeHost(mail);
     if (side) cudaStreamDestroy(side);
     if (hi) cudaStreamDestroy(hi);
@@ -929,6 +942,18 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
     doff[q] = tot;
     off_dense0[lf] = tot;
     tot += (long long)h * w;
+  }
+  H->nf_r0 = dr0;
+  H->nf_c0 = dc0;
+  H->nf_h = dh;
+  {
+    // row clusters of the row tree's leaves (they partition [0, n_rows))
+    std::vector<int> st;
+    for (int64_t q = 0; q < d->n_row_nodes; ++q)
+      if (d->row_nodes[5 * q + 3] < 0) st.push_back((int)d->row_nodes[5 * q]);
+    std::sort(st.begin(), st.end());
+    st.push_back(H->n_rows);
+    H->rleaf_start = st;
   }
   H->nf_entries = tot;
   {
@@ -1808,65 +1833,140 @@ int hbem_hmat_copy_arenas(const hbem_hmat *hc, void *u, void *v, void *dense) {
   return HBEM_OK;
 }
 
-int hbem_hmat_matvec(const hbem_hmat *hc, const void *x, void *y) {
-  clear_error();
-  hbem_hmat *h = const_cast<hbem_hmat *>(hc);
-  if (!h || !x || !y) return set_error(HBEM_ERR_ARG, "null argument");
-  HB_CUDA(cudaSetDevice(h->device));
+// build the matvec's work items, slot layout and cover lists once per
+// assembly (host lists from the last execute, uploaded)
+static int matvec_prepare(hbem_hmat *h) {
+  if (!h->mv_dirty) return HBEM_OK;
+  const size_t vb = h->vbytes;
+  cudaFree(h->mv_ad); cudaFree(h->mv_ad_l);
+  h->mv_ad = nullptr; h->mv_ad_l = nullptr;
+  const size_t na = h->ad_r0.size();
+  HB_CUDA(cudaMalloc(&h->mv_ad, std::max<size_t>(na, 1) * 4 * 4));
+  HB_CUDA(cudaMalloc(&h->mv_ad_l, std::max<size_t>(na, 1) * 8 * 2));
+  if (na) {
+    HB_CUDA(cudaMemcpy(h->mv_ad, h->ad_r0.data(), na * 4, cudaMemcpyHostToDevice));
+    HB_CUDA(cudaMemcpy(h->mv_ad + na, h->ad_c0.data(), na * 4, cudaMemcpyHostToDevice));
+    HB_CUDA(cudaMemcpy(h->mv_ad + 2 * na, h->ad_h.data(), na * 4, cudaMemcpyHostToDevice));
+    HB_CUDA(cudaMemcpy(h->mv_ad + 3 * na, h->ad_w.data(), na * 4, cudaMemcpyHostToDevice));
+    HB_CUDA(cudaMemcpy(h->mv_ad_l, h->ad_off.data(), na * 8, cudaMemcpyHostToDevice));
+    HB_CUDA(cudaMemcpy(h->mv_ad_l + na, h->ad_rowbase.data(), na * 8, cudaMemcpyHostToDevice));
+  }
+  long long ad_rows = 0;
+  for (int hh : h->ad_h) ad_rows += hh;
+  h->mv_ad_rows = ad_rows;
+  // low-rank work items: (list position, chunk start) over columns (dots)
+  // and rows, kMvChunk each; per-position offsets of the k dots
+  cudaFree(h->mv_items); cudaFree(h->mv_sbase); cudaFree(h->mv_s);
+  cudaFree(h->mv_part); cudaFree(h->mv_dpart);
+  cudaFree(h->mv_ifirst); cudaFree(h->mv_ibase); cudaFree(h->mv_rbase);
+  cudaFree(h->mv_cstart); cudaFree(h->mv_cptr); cudaFree(h->mv_cover);
+  h->mv_items = nullptr; h->mv_sbase = nullptr; h->mv_s = nullptr;
+  h->mv_part = h->mv_dpart = nullptr;
+  h->mv_ifirst = h->mv_ibase = h->mv_rbase = nullptr;
+  h->mv_cstart = nullptr; h->mv_cptr = h->mv_cover = nullptr;
+  const int nl = h->n_lowrank;
+  std::vector<int> lst(nl), rk(h->na > 0 ? h->na : 1);
+  if (nl > 0) {
+    HB_CUDA(cudaMemcpy(lst.data(), h->lr_list, (size_t)nl * 4, cudaMemcpyDeviceToHost));
+    HB_CUDA(cudaMemcpy(rk.data(), h->S.rank, (size_t)h->na * 4, cudaMemcpyDeviceToHost));
+  }
+  const long long lr0 = h->nf_rows + ad_rows;  // first low-rank partial slot
+  std::vector<int2> items;
+  std::vector<long long> sbase(std::max(nl, 1)), ifirst(nl + 1), ibase, rbase(std::max(nl, 1));
+  long long ns = 0, nsd = 0, rows = lr0;
+  for (int p = 0; p < nl; ++p) {
+    const int b = lst[p];
+    sbase[p] = ns;
+    ns += rk[b];
+    rbase[p] = rows;
+    rows += h->ah[b];
+    ifirst[p] = (long long)items.size();
+    for (int c = 0; c < h->aw[b]; c += kMvChunk) {
+      items.push_back(make_int2(p, c));
+      ibase.push_back(nsd);
+      nsd += rk[b];
+    }
+  }
+  ifirst[nl] = (long long)items.size();
+  const long long nd_items = (long long)items.size();
+  for (int p = 0; p < nl; ++p)
+    for (int r = 0; r < h->ah[lst[p]]; r += kMvChunk) items.push_back(make_int2(p, r));
+  h->mv_nd = nd_items;
+  h->mv_nr = (long long)items.size() - nd_items;
+  h->mv_ns = ns;
+  const long long nslots = rows;
+  // cover lists: every leaf component (near-field leaf, admissible block
+  // stored densely, low-rank block) in the reference's (row start, column
+  // start) order, appended to each tree row cluster inside its row range
+  struct Comp { int r0, c0, h; long long cover; };
+  std::vector<Comp> comps;
+  comps.reserve((size_t)h->nd + na + nl);
+  {
+    long long acc = 0;  // near-field leaf rows: exclusive prefix of the heights (nf_rowbase)
+    for (int q = 0; q < h->nd; ++q) {
+      comps.push_back({h->nf_r0[q], h->nf_c0[q], h->nf_h[q], acc - h->nf_r0[q]});
+      acc += h->nf_h[q];
+    }
+  }
+  for (size_t z = 0; z < na; ++z)
+    comps.push_back({h->ad_r0[z], h->ad_c0[z], h->ad_h[z],
+                     h->nf_rows + h->ad_rowbase[z] - h->ad_r0[z]});
+  for (int p = 0; p < nl; ++p) {
+    const int b = lst[p];
+    comps.push_back({h->ar0[b], h->ac0[b], h->ah[b], rbase[p] - h->ar0[b]});
+  }
+  std::sort(comps.begin(), comps.end(), [](const Comp &a, const Comp &b) {
+    return a.r0 != b.r0 ? a.r0 < b.r0 : a.c0 < b.c0;
+  });
+  const std::vector<int> &cs = h->rleaf_start;
+  const int ncl = (int)cs.size() - 1;
+  std::vector<long long> cnt(ncl + 1, 0);
+  auto cl_of = [&](int r) {  // row cluster containing row r
+    return (int)(std::upper_bound(cs.begin(), cs.end(), r) - cs.begin()) - 1;
+  };
+  for (const Comp &c : comps)
+    for (int g = cl_of(c.r0); g < ncl && cs[g] < c.r0 + c.h; ++g) ++cnt[g];
+  std::vector<long long> cptr(ncl + 1, 0);
+  for (int g = 0; g < ncl; ++g) cptr[g + 1] = cptr[g] + cnt[g];
+  std::vector<long long> cover((size_t)std::max<long long>(cptr[ncl], 1));
+  std::vector<long long> fill(cptr.begin(), cptr.end() - 1);
+  for (const Comp &c : comps)
+    for (int g = cl_of(c.r0); g < ncl && cs[g] < c.r0 + c.h; ++g) cover[fill[g]++] = c.cover;
+  h->mv_ncl = ncl;
+  HB_CUDA(cudaMalloc(&h->mv_items, std::max<size_t>(items.size(), 1) * sizeof(int2)));
+  HB_CUDA(cudaMalloc(&h->mv_sbase, sbase.size() * 8));
+  HB_CUDA(cudaMalloc(&h->mv_s, (size_t)std::max<long long>(ns, 1) * vb));
+  HB_CUDA(cudaMalloc(&h->mv_dpart, (size_t)std::max<long long>(nsd, 1) * vb));
+  HB_CUDA(cudaMalloc(&h->mv_part, (size_t)std::max<long long>(nslots, 1) * vb));
+  HB_CUDA(cudaMalloc(&h->mv_ifirst, ifirst.size() * 8));
+  HB_CUDA(cudaMalloc(&h->mv_ibase, std::max<size_t>(ibase.size(), 1) * 8));
+  HB_CUDA(cudaMalloc(&h->mv_rbase, rbase.size() * 8));
+  HB_CUDA(cudaMalloc(&h->mv_cstart, cs.size() * 4));
+  HB_CUDA(cudaMalloc(&h->mv_cptr, cptr.size() * 8));
+  HB_CUDA(cudaMalloc(&h->mv_cover, cover.size() * 8));
+  if (!items.empty())
+    HB_CUDA(cudaMemcpy(h->mv_items, items.data(), items.size() * sizeof(int2),
+                       cudaMemcpyHostToDevice));
+  HB_CUDA(cudaMemcpy(h->mv_sbase, sbase.data(), sbase.size() * 8, cudaMemcpyHostToDevice));
+  HB_CUDA(cudaMemcpy(h->mv_ifirst, ifirst.data(), ifirst.size() * 8, cudaMemcpyHostToDevice));
+  if (!ibase.empty())
+    HB_CUDA(cudaMemcpy(h->mv_ibase, ibase.data(), ibase.size() * 8, cudaMemcpyHostToDevice));
+  HB_CUDA(cudaMemcpy(h->mv_rbase, rbase.data(), rbase.size() * 8, cudaMemcpyHostToDevice));
+  HB_CUDA(cudaMemcpy(h->mv_cstart, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+  HB_CUDA(cudaMemcpy(h->mv_cptr, cptr.data(), cptr.size() * 8, cudaMemcpyHostToDevice));
+  HB_CUDA(cudaMemcpy(h->mv_cover, cover.data(), cover.size() * 8, cudaMemcpyHostToDevice));
+  h->mv_dirty = false;
+  return HBEM_OK;
+}
+
+// y = H x with x, y device pointers in the original DOF order, on stream st
+static int matvec_device(hbem_hmat *h, const void *dx, void *dy, cudaStream_t st) {
   const size_t vb = h->vbytes;
   const int nr = h->n_rows, nc = h->n_cols;
   if (!h->mv_buf) HB_CUDA(cudaMalloc(&h->mv_buf, (size_t)2 * (nr + nc) * vb));
   char *buf = static_cast<char *>(h->mv_buf);
-  void *dx = buf, *dxt = buf + (size_t)nc * vb, *dy = buf + (size_t)2 * nc * vb,
-       *dyt = buf + (size_t)(2 * nc + nr) * vb;
-  if (h->mv_dirty) {
-    cudaFree(h->mv_ad); cudaFree(h->mv_ad_l);
-    h->mv_ad = nullptr; h->mv_ad_l = nullptr;
-    const size_t na = h->ad_r0.size();
-    HB_CUDA(cudaMalloc(&h->mv_ad, std::max<size_t>(na, 1) * 4 * 4));
-    HB_CUDA(cudaMalloc(&h->mv_ad_l, std::max<size_t>(na, 1) * 8 * 2));
-    if (na) {
-      HB_CUDA(cudaMemcpy(h->mv_ad, h->ad_r0.data(), na * 4, cudaMemcpyHostToDevice));
-      HB_CUDA(cudaMemcpy(h->mv_ad + na, h->ad_c0.data(), na * 4, cudaMemcpyHostToDevice));
-      HB_CUDA(cudaMemcpy(h->mv_ad + 2 * na, h->ad_h.data(), na * 4, cudaMemcpyHostToDevice));
-      HB_CUDA(cudaMemcpy(h->mv_ad + 3 * na, h->ad_w.data(), na * 4, cudaMemcpyHostToDevice));
-      HB_CUDA(cudaMemcpy(h->mv_ad_l, h->ad_off.data(), na * 8, cudaMemcpyHostToDevice));
-      HB_CUDA(cudaMemcpy(h->mv_ad_l + na, h->ad_rowbase.data(), na * 8, cudaMemcpyHostToDevice));
-    }
-    // low-rank work items: (list position, chunk start) over columns (dots)
-    // and rows, kMvChunk each; per-position offsets of the k dots
-    cudaFree(h->mv_items); cudaFree(h->mv_sbase); cudaFree(h->mv_s);
-    h->mv_items = nullptr; h->mv_sbase = nullptr; h->mv_s = nullptr;
-    const int nl = h->n_lowrank;
-    std::vector<int> lst(nl), rk(h->na > 0 ? h->na : 1);
-    if (nl > 0) {
-      HB_CUDA(cudaMemcpy(lst.data(), h->lr_list, (size_t)nl * 4, cudaMemcpyDeviceToHost));
-      HB_CUDA(cudaMemcpy(rk.data(), h->S.rank, (size_t)h->na * 4, cudaMemcpyDeviceToHost));
-    }
-    std::vector<int2> items;
-    std::vector<long long> sbase(std::max(nl, 1));
-    long long ns = 0;
-    for (int p = 0; p < nl; ++p) {
-      const int b = lst[p];
-      sbase[p] = ns;
-      ns += rk[b];
-      for (int c = 0; c < h->aw[b]; c += kMvChunk) items.push_back(make_int2(p, c));
-    }
-    const long long nd_items = (long long)items.size();
-    for (int p = 0; p < nl; ++p)
-      for (int r = 0; r < h->ah[lst[p]]; r += kMvChunk) items.push_back(make_int2(p, r));
-    h->mv_nd = nd_items;
-    h->mv_nr = (long long)items.size() - nd_items;
-    h->mv_ns = ns;
-    HB_CUDA(cudaMalloc(&h->mv_items, std::max<size_t>(items.size(), 1) * sizeof(int2)));
-    HB_CUDA(cudaMalloc(&h->mv_sbase, sbase.size() * 8));
-    HB_CUDA(cudaMalloc(&h->mv_s, (size_t)std::max<long long>(ns, 1) * vb));
-    if (!items.empty())
-      HB_CUDA(cudaMemcpy(h->mv_items, items.data(), items.size() * sizeof(int2),
-                         cudaMemcpyHostToDevice));
-    HB_CUDA(cudaMemcpy(h->mv_sbase, sbase.data(), sbase.size() * 8, cudaMemcpyHostToDevice));
-    h->mv_dirty = false;
-  }
+  void *dxt = buf + (size_t)nc * vb, *dyt = buf + (size_t)(2 * nc + nr) * vb;
+  HB_CHECK(matvec_prepare(h));
   MatvecArgs M{};
   M.n_rows = nr;
   M.n_cols = nc;
@@ -1874,16 +1974,14 @@ int hbem_hmat_matvec(const hbem_hmat *hc, const void *x, void *y) {
   M.cperm = h->cperm;
   M.x = dx; M.y = dy; M.xt = dxt; M.yt = dyt;
   M.dense[0] = MatvecArgs::Dense{h->nd, h->D.r0, h->D.c0, h->D.h, h->D.w, h->D.off,
-                                 h->nf_rowbase, h->nf_rows, h->dense_nf};
+                                 h->nf_rowbase, h->nf_rows, h->dense_nf, 0};
   const int na = (int)h->ad_r0.size();
-  long long ad_rows = 0;
-  for (int hh : h->ad_h) ad_rows += hh;
   M.dense[1] = MatvecArgs::Dense{na, h->mv_ad, h->mv_ad + na, h->mv_ad + 2 * na,
-                                 h->mv_ad + 3 * na, h->mv_ad_l, h->mv_ad_l + na, ad_rows,
-                                 h->dense_adm};
+                                 h->mv_ad + 3 * na, h->mv_ad_l, h->mv_ad_l + na, h->mv_ad_rows,
+                                 h->dense_adm, h->nf_rows};
   M.n_lowrank = h->n_lowrank;
   M.lowrank = h->lr_list;
-  HB_CHECK(ensure_packed(h, 0));
+  HB_CHECK(ensure_packed(h, st));
   M.ua = reinterpret_cast<const void *>(h->uarena.base);
   M.va = reinterpret_cast<const void *>(h->varena.base);
   M.uoff = h->blk_uoff;
@@ -1893,18 +1991,47 @@ int hbem_hmat_matvec(const hbem_hmat *hc, const void *x, void *y) {
   M.ditems = h->mv_items;
   M.ritems = h->mv_items + h->mv_nd;
   M.sbase = h->mv_sbase;
+  M.ifirst = h->mv_ifirst;
+  M.ibase = h->mv_ibase;
+  M.rbase = h->mv_rbase;
   M.s = h->mv_s;
+  M.dpart = h->mv_dpart;
   M.n_s = h->mv_ns;
-  HB_CUDA(cudaMemcpy(dx, x, (size_t)nc * vb, cudaMemcpyHostToDevice));
+  M.part = h->mv_part;
+  M.n_clusters = h->mv_ncl;
+  M.cstart = h->mv_cstart;
+  M.cptr = h->mv_cptr;
+  M.cover = h->mv_cover;
   const hbem_ctx *ctx = h->ctx;
-  int rc;
   if (ctx->precision == HBEM_DOUBLE)
-    rc = ctx->helm ? matvec_launch<double, true>(M, h->S, 0) : matvec_launch<double, false>(M, h->S, 0);
-  else
-    rc = ctx->helm ? matvec_launch<float, true>(M, h->S, 0) : matvec_launch<float, false>(M, h->S, 0);
-  if (rc != HBEM_OK) return rc;
+    return ctx->helm ? matvec_launch<double, true>(M, h->S, st)
+                     : matvec_launch<double, false>(M, h->S, st);
+  return ctx->helm ? matvec_launch<float, true>(M, h->S, st)
+                   : matvec_launch<float, false>(M, h->S, st);
+}
+
+int hbem_hmat_matvec(const hbem_hmat *hc, const void *x, void *y) {
+  clear_error();
+  hbem_hmat *h = const_cast<hbem_hmat *>(hc);
+  if (!h || !x || !y) return set_error(HBEM_ERR_ARG, "null argument");
+  HB_CUDA(cudaSetDevice(h->device));
+  const size_t vb = h->vbytes;
+  const int nr = h->n_rows, nc = h->n_cols;
+  if (!h->mv_buf) HB_CUDA(cudaMalloc(&h->mv_buf, (size_t)2 * (nr + nc) * vb));
+  char *buf = static_cast<char *>(h->mv_buf);
+  void *dx = buf, *dy = buf + (size_t)2 * nc * vb;
+  HB_CUDA(cudaMemcpy(dx, x, (size_t)nc * vb, cudaMemcpyHostToDevice));
+  HB_CHECK(matvec_device(h, dx, dy, 0));
   HB_CUDA(cudaMemcpy(y, dy, (size_t)nr * vb, cudaMemcpyDeviceToHost));
   return HBEM_OK;
+}
+
+int hbem_hmat_matvec_device(const hbem_hmat *hc, const void *d_x, void *d_y, void *stream) {
+  clear_error();
+  hbem_hmat *h = const_cast<hbem_hmat *>(hc);
+  if (!h || !d_x || !d_y) return set_error(HBEM_ERR_ARG, "null argument");
+  HB_CUDA(cudaSetDevice(h->device));
+  return matvec_device(h, d_x, d_y, (cudaStream_t)stream);
 }
 
 int hbem_hmat_destroy(hbem_hmat *h) {

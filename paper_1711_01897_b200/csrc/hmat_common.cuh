@@ -566,6 +566,7 @@ struct MatvecArgs {
     const long long *off, *rowbase;
     long long nrows;
     const void *arena;
+    long long part_base;  // first partial slot of this list (leaf row g -> part_base + g)
   } dense[2];     // near-field leaves, admissible blocks stored densely
   int n_lowrank;
   const int *lowrank;  // admissible block slots
@@ -577,9 +578,21 @@ struct MatvecArgs {
   // columns each, so one huge block does not serialise on one warp
   long long n_ditems, n_ritems;
   const int2 *ditems, *ritems;
-  const long long *sbase;  // per list position: offset of its k dots in s
-  void *s;                 // sum_k complex/real dots (zeroed per matvec)
+  const long long *sbase;   // per list position: offset of its k dots in s
+  const long long *ifirst;  // per list position: first dots item (n_lowrank + 1)
+  const long long *ibase;   // per dots item: offset of its k partial dots in dpart
+  const long long *rbase;   // per list position: first partial slot of its rows
+  void *s;                  // per-block dots
+  void *dpart;              // per-chunk partial dots
   long long n_s;
+  // deterministic reduction: every leaf's row contributions in private slots
+  // (part), summed per row over the covering leaves in the reference's
+  // (row start, column start) order, one warp per row cluster of the tree
+  void *part;
+  int n_clusters;
+  const int *cstart;        // n_clusters + 1 row-cluster starts
+  const long long *cptr;    // n_clusters + 1 offsets into cover
+  const long long *cover;   // slot base minus the leaf's first row
 };
 constexpr int kMvChunk = 512;
 template <typename T, bool C>

@@ -1,25 +1,19 @@
 // Device H-matrix matvec y = H x (hmat_matvec, hmatrix.py:441-470) straight
 // from the device arenas: dense leaves row by row, low-rank blocks from the
 // packed U / V arenas (contiguous per block; the ACA pool scatters a block's
-// terms over one region per wave, which costs a TLB miss per term).  Leaf contributions are
-// accumulated with atomics (the sum order over leaves is not fixed, so
-// results agree with the host matvec to rounding, not bitwise).
+// terms over one region per wave, which costs a TLB miss per term).
+//
+// Bit-reproducible like the reference ("leaves are applied sequentially in a
+// fixed (row, column) order, so the result is reproducible bit for bit
+// between calls"): no float atomics.  Every leaf writes its own row
+// contributions into a private slot range (partials), chunked low-rank dots
+// are summed per block in chunk order, and one warp per row cluster of the
+// tree adds, for each of its rows, the contributions of the leaves covering
+// it in the reference's (row start, column start) order.
 #pragma once
 #include "hmat_common.cuh"
 
 namespace hb {
-
-template <typename V> __device__ __forceinline__ void atomic_add_v(V *p, V v);
-template <> __device__ __forceinline__ void atomic_add_v<double>(double *p, double v) { atomicAdd(p, v); }
-template <> __device__ __forceinline__ void atomic_add_v<float>(float *p, float v) { atomicAdd(p, v); }
-template <> __device__ __forceinline__ void atomic_add_v<Cx<double>>(Cx<double> *p, Cx<double> v) {
-  atomicAdd(&p->re, v.re);
-  atomicAdd(&p->im, v.im);
-}
-template <> __device__ __forceinline__ void atomic_add_v<Cx<float>>(Cx<float> *p, Cx<float> v) {
-  atomicAdd(&p->re, v.re);
-  atomicAdd(&p->im, v.im);
-}
 
 template <typename T, bool C>
 __device__ __forceinline__ typename Num<T, C>::V warp_sum_v(typename Num<T, C>::V v) {
@@ -41,7 +35,7 @@ __device__ __forceinline__ typename Num<T, C>::V warp_sum_v(typename Num<T, C>::
 template <typename T, bool C>
 __global__ void k_mv_dense(int nl, const int *r0, const int *c0, const int *h, const int *w,
                            const long long *off, const long long *rowbase, long long nrows,
-                           const void *arena, const void *xt, void *yt) {
+                           const void *arena, const void *xt, void *part) {
   using N = Num<T, C>;
   using V = typename N::V;
   const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -59,7 +53,7 @@ __global__ void k_mv_dense(int nl, const int *r0, const int *c0, const int *h, c
   V acc = N::zero();
   for (int c = lane; c < ww; c += 32) acc = N::fma_acc(acc, A[c], x[c]);
   acc = warp_sum_v<T, C>(acc);
-  if (lane == 0) atomic_add_v<V>(static_cast<V *>(yt) + r0[s] + i, acc);
+  if (lane == 0) static_cast<V *>(part)[g] = acc;  // slot: leaf row g of this list
 }
 
 // one warp per low-rank block: s_l = v_l . x, y += sum_l u_l s_l.  The term
@@ -82,8 +76,8 @@ __device__ __forceinline__ typename Num<T, C>::V shfl_v(typename Num<T, C>::V v,
 //   rows: warp per (block, <= kMvChunk rows):    y[chunk] += sum_l u_l[chunk] s_l
 template <typename T, bool C>
 __global__ void k_mv_dots(long long n, const int2 *items, const int *slots, AcaDev S,
-                          const void *va, const long long *voff, const long long *sbase,
-                          const void *xt, void *s) {
+                          const void *va, const long long *voff, const long long *ibase,
+                          const void *xt, void *dpart) {
   using N = Num<T, C>;
   using V = typename N::V;
   const long long it = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -95,7 +89,7 @@ __global__ void k_mv_dots(long long n, const int2 *items, const int *slots, AcaD
   const int c0 = wi.y, c1 = min(w, c0 + kMvChunk);
   const V *W = static_cast<const V *>(va) + voff[b];  // column l: W[l * w + c]
   const V *x = static_cast<const V *>(xt) + S.c0[b];
-  V *sd = static_cast<V *>(s) + sbase[wi.x];
+  V *sd = static_cast<V *>(dpart) + ibase[it];  // this chunk's k partial dots
   for (int l = 0; l < k; l += 4) {
     V acc[4];
 #pragma unroll
@@ -109,15 +103,37 @@ __global__ void k_mv_dots(long long n, const int2 *items, const int *slots, AcaD
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const V d = warp_sum_v<T, C>(acc[u]);
-      if (lane == 0 && l + u < k) atomic_add_v<V>(sd + l + u, d);
+      if (lane == 0 && l + u < k) sd[l + u] = d;
     }
+  }
+}
+
+// dots of list position p: sum of its chunks' partial dots in chunk order
+template <typename T, bool C>
+__global__ void k_mv_dots_sum(int nl, const int *slots, AcaDev S, const long long *sbase,
+                              const long long *ifirst, const long long *ibase,
+                              const void *dpart, void *s) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  const int p = blockIdx.x * (blockDim.x / 8) + threadIdx.x / 8;
+  if (p >= nl) return;
+  const int k = S.rank[slots[p]];
+  const V *dp = static_cast<const V *>(dpart);
+  for (int l = threadIdx.x % 8; l < k; l += 8) {
+    V acc = N::zero();
+    for (long long it = ifirst[p]; it < ifirst[p + 1]; ++it) {
+      const V d = dp[ibase[it] + l];
+      if constexpr (C) { acc.re += d.re; acc.im += d.im; }
+      else acc += d;
+    }
+    static_cast<V *>(s)[sbase[p] + l] = acc;
   }
 }
 
 template <typename T, bool C>
 __global__ void k_mv_rows(long long n, const int2 *items, const int *slots, AcaDev S,
                           const void *ua, const long long *uoff, const long long *sbase,
-                          const void *s, void *yt) {
+                          const void *s, const long long *rbase, void *part) {
   using N = Num<T, C>;
   using V = typename N::V;
   const long long it = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -129,21 +145,44 @@ __global__ void k_mv_rows(long long n, const int2 *items, const int *slots, AcaD
   const int r0 = wi.y, r1 = min(h, r0 + kMvChunk);
   const V *U = static_cast<const V *>(ua) + uoff[b];  // column l: U[l * h + i]
   const V *sd = static_cast<const V *>(s) + sbase[wi.x];
-  V *y = static_cast<V *>(yt) + S.r0[b];
-  for (int l0 = 0; l0 < k; l0 += 32) {
-    const int lk = min(32, k - l0);
-    const V mine = lane < lk ? sd[l0 + lane] : N::zero();
-    for (int i0 = r0; i0 < r1; i0 += 32) {  // warp-uniform trip count (shuffles)
-      const int i = i0 + lane;
-      V acc = N::zero();
+  V *y = static_cast<V *>(part) + rbase[wi.x];  // this block's row slots
+  for (int i0 = r0; i0 < r1; i0 += 32) {  // warp-uniform trip count (shuffles)
+    const int i = i0 + lane;
+    V acc = N::zero();
+    for (int l0 = 0; l0 < k; l0 += 32) {
+      const int lk = min(32, k - l0);
+      const V mine = lane < lk ? sd[l0 + lane] : N::zero();
 #pragma unroll 4
       for (int l = 0; l < lk; ++l) {
         const V sl = shfl_v<T, C>(mine, l);
         if (i < r1) acc = N::fma_acc(acc, U[(long long)(l0 + l) * h + i], sl);
       }
-      if (i < r1) atomic_add_v<V>(y + i, acc);
     }
+    if (i < r1) y[i] = acc;
   }
+}
+
+// one warp per row cluster [cs, ce) of the tree (<= 32 rows): row r adds the
+// contributions of the leaves covering it, cover list = slot bases minus the
+// leaf's first row, in the reference's (row start, column start) order
+template <typename T, bool C>
+__global__ void k_mv_reduce(int ncl, const int *cstart, const long long *cptr,
+                            const long long *cover, const void *part, void *yt) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= ncl) return;
+  const int r = cstart[g] + lane;
+  if (r >= cstart[g + 1]) return;
+  const V *pp = static_cast<const V *>(part);
+  V acc = N::zero();
+  for (long long j = cptr[g]; j < cptr[g + 1]; ++j) {
+    const V d = pp[cover[j] + r];
+    if constexpr (C) { acc.re += d.re; acc.im += d.im; }
+    else acc += d;
+  }
+  static_cast<V *>(yt)[r] = acc;
 }
 
 template <typename T, bool C>
@@ -161,23 +200,26 @@ __global__ void k_mv_scatter(int n, const int *perm, const void *yt, void *y) {
 
 template <typename T, bool C>
 int matvec_launch(const MatvecArgs &M, const AcaDev &S, cudaStream_t st) {
-  const size_t vb = sizeof(typename Num<T, C>::V);
-  HB_CUDA(cudaMemsetAsync(M.yt, 0, (size_t)M.n_rows * vb, st));
+  using V = typename Num<T, C>::V;
   k_mv_gather<T, C><<<(M.n_cols + 255) / 256, 256, 0, st>>>(M.n_cols, M.cperm, M.x, M.xt);
   for (int a = 0; a < 2; ++a) {
     const MatvecArgs::Dense &D = M.dense[a];
     if (D.n <= 0 || D.nrows <= 0) continue;
     const long long warps = D.nrows;
     k_mv_dense<T, C><<<(unsigned)((warps + 3) / 4), 128, 0, st>>>(
-        D.n, D.r0, D.c0, D.h, D.w, D.off, D.rowbase, D.nrows, D.arena, M.xt, M.yt);
+        D.n, D.r0, D.c0, D.h, D.w, D.off, D.rowbase, D.nrows, D.arena, M.xt,
+        static_cast<V *>(M.part) + D.part_base);
   }
   if (M.n_lowrank > 0) {
-    HB_CUDA(cudaMemsetAsync(M.s, 0, (size_t)std::max<long long>(M.n_s, 1) * vb, st));
     k_mv_dots<T, C><<<(unsigned)((M.n_ditems + 3) / 4), 128, 0, st>>>(
-        M.n_ditems, M.ditems, M.lowrank, S, M.va, M.voff, M.sbase, M.xt, M.s);
+        M.n_ditems, M.ditems, M.lowrank, S, M.va, M.voff, M.ibase, M.xt, M.dpart);
+    k_mv_dots_sum<T, C><<<(unsigned)((M.n_lowrank + 15) / 16), 128, 0, st>>>(
+        M.n_lowrank, M.lowrank, S, M.sbase, M.ifirst, M.ibase, M.dpart, M.s);
     k_mv_rows<T, C><<<(unsigned)((M.n_ritems + 3) / 4), 128, 0, st>>>(
-        M.n_ritems, M.ritems, M.lowrank, S, M.ua, M.uoff, M.sbase, M.s, M.yt);
+        M.n_ritems, M.ritems, M.lowrank, S, M.ua, M.uoff, M.sbase, M.s, M.rbase, M.part);
   }
+  k_mv_reduce<T, C><<<(unsigned)((M.n_clusters + 3) / 4), 128, 0, st>>>(
+      M.n_clusters, M.cstart, M.cptr, M.cover, M.part, M.yt);
   k_mv_scatter<T, C><<<(M.n_rows + 255) / 256, 256, 0, st>>>(M.n_rows, M.rperm, M.yt, M.y);
   HB_CUDA(cudaGetLastError());
   return HBEM_OK;

@@ -247,6 +247,12 @@ class _DevicePart:
         check(lib.hbem_hmat_matvec(self.handle, _lib.vptr(x), _lib.vptr(y)))
         return y
 
+    def matvec_device(self, x_ptr: int, y_ptr: int, stream=None) -> None:
+        """y = H_part x on device pointers (original DOF order, result dtype),
+        enqueued on ``stream``; bit-reproducible between calls."""
+        check(lib.hbem_hmat_matvec_device(self.handle, C.c_void_p(x_ptr), C.c_void_p(y_ptr),
+                                          stream))
+
     def close(self):
         if self.handle:
             lib.hbem_hmat_destroy(self.handle)
@@ -281,6 +287,23 @@ class HMatrix:
     def matvec(self, x):
         return hmat_matvec(self, x)
 
+    def matvec_torch(self, x):
+        """y = H x for a CUDA torch vector (original DOF order), on the
+        current torch stream: device matvec of every part (bit-reproducible),
+        parts summed in part order.  The result has the H-matrix dtype."""
+        import torch
+        tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32,
+               np.dtype(np.complex128): torch.complex128,
+               np.dtype(np.complex64): torch.complex64}[np.dtype(self.dtype)]
+        xc = x.to(tdt).contiguous()
+        stream = torch.cuda.current_stream(xc.device).cuda_stream
+        y = None
+        for _, part in self.parts:
+            yp = torch.empty(self.shape[0], dtype=tdt, device=xc.device)
+            part.matvec_device(xc.data_ptr(), yp.data_ptr(), stream)
+            y = yp if y is None else y + yp
+        return y
+
     def to_dense(self):
         m, n = self.shape
         out = np.zeros((m, n), dtype=self.dtype)
@@ -304,11 +327,15 @@ def hmat_matvec(h: HMatrix, x: np.ndarray, device: bool = True) -> np.ndarray:
     x = np.asarray(x)
     if x.shape != (n,):
         raise AssemblyError(f"matvec expects a vector of length {n}, got {x.shape}")
-    if device and h.parts and all(p.handle for _, p in h.parts):
-        rd = np.dtype(h.dtype)
-        if np.iscomplexobj(x) and rd.kind != "c":
-            return (hmat_matvec(h, x.real.copy(), True)
-                    + 1j * hmat_matvec(h, x.imag.copy(), True))
+    rd = np.dtype(h.dtype)
+    if device and np.iscomplexobj(x) and rd.kind != "c":
+        return (hmat_matvec(h, x.real.copy(), True)
+                + 1j * hmat_matvec(h, x.imag.copy(), True))
+    # the device applies the payloads in their own precision; a wider x
+    # (float64 into a float32 H-matrix) promotes like the reference
+    # (np.result_type(h.dtype, x.dtype)) on the host leaf loop below
+    if device and np.result_type(rd, x.dtype) == rd and h.parts and \
+            all(p.handle for _, p in h.parts):
         y = None
         for _, part in h.parts:
             yp = part.matvec(x.astype(rd, copy=False))

@@ -24,6 +24,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 import scipy.sparse as sps
+import torch
 
 from . import _lib
 from ._lib import check, lib
@@ -322,7 +323,7 @@ def burton_miller_solve(cfg: ScatterConfig, wave: PlaneWave | None = None, mode:
     from .discretization import OperatorSpec, build_space, make_integration_context
     from .hmatrix import assemble_hmatrix
     from .partition import cluster_trees_for
-    from .solvers import gmres
+    from .solvers import GmresResult, gmres
 
     if mode not in ("dense", "hmatrix"):
         raise ConfigError(f"mode must be 'dense' or 'hmatrix', got {mode!r}")
@@ -343,6 +344,10 @@ def burton_miller_solve(cfg: ScatterConfig, wave: PlaneWave | None = None, mode:
     qt, pt = [q.T.tocsr() for q in qm], [p.T.tocsr() for p in pm]
     spec_k = OperatorSpec("helmholtz", "dlp", k)
     spec_s = OperatorSpec("helmholtz", "slp", k)
+    # the solve runs on the GPU: operators applied by device matvecs (H-matrix
+    # mode) or dense products, the sparse mass / surface-curl / normal maps as
+    # cuSPARSE CSR products, the GMRES basis in HBM
+    dev = torch.device("cuda", torch.cuda.current_device())
     if mode == "dense":
         from .assembly import assemble_dense
         n_dev = cfg.assembly.devices or 1
@@ -354,31 +359,49 @@ def burton_miller_solve(cfg: ScatterConfig, wave: PlaneWave | None = None, mode:
         s_op = assemble_dense(spec_s, p1d, p1d, cfg.assembly,
                               make_gpu_backends(make_integration_context(spec_s, p1d, p1d,
                                                                          **orders), n_dev))
-        apply_k, apply_s = k_op.__matmul__, s_op.__matmul__
+        k_d = torch.from_numpy(k_op).to(dev)
+        s_d = torch.from_numpy(s_op).to(dev)
+        apply_k, apply_s = k_d.__matmul__, s_d.__matmul__
     else:
         k_op = assemble_hmatrix(spec_k, p1c, p1c, cluster_trees_for(p1c, p1c, cfg.n_min, cfg.eta),
                                 cfg.aca, assembly_config=cfg.assembly)
         s_op = assemble_hmatrix(spec_s, p1d, p1d, cluster_trees_for(p1d, p1d, cfg.n_min, cfg.eta),
                                 cfg.aca, assembly_config=cfg.assembly)
-        apply_k, apply_s = k_op.matvec, s_op.matvec
+        apply_k, apply_s = k_op.matvec_torch, s_op.matvec_torch
     eta_c = 1.0 / (1j * k)
 
+    def csr(a):
+        a = a.tocsr()
+        return torch.sparse_csr_tensor(torch.from_numpy(a.indptr.astype(np.int64)),
+                                       torch.from_numpy(a.indices.astype(np.int64)),
+                                       torch.from_numpy(a.data.astype(np.complex128)),
+                                       size=a.shape, check_invariants=False).to(dev)
+
+    with warnings.catch_warnings():  # torch marks CSR "beta"
+        warnings.simplefilter("ignore", UserWarning)
+        mass_d = csr(mass)
+        qm_d, qt_d = [csr(q) for q in qm], [csr(q) for q in qt]
+        pm_d, pt_d = [csr(p) for p in pm], [csr(p) for p in pt]
+
     def apply_d(x):
-        curl = np.zeros(p1c.n_dofs, np.complex128)
-        for q, qq in zip(qm, qt):
-            curl += qq @ apply_s(q @ x)
-        norm = np.zeros(p1c.n_dofs, np.complex128)
-        for p, pp in zip(pm, pt):
-            norm += pp @ apply_s(p @ x)
+        curl = torch.zeros(p1c.n_dofs, dtype=torch.complex128, device=dev)
+        for q, qq in zip(qm_d, qt_d):
+            curl += qq @ apply_s(q @ x).to(torch.complex128)
+        norm = torch.zeros_like(curl)
+        for p, pp in zip(pm_d, pt_d):
+            norm += pp @ apply_s(p @ x).to(torch.complex128)
         return curl - k * k * norm
 
     def operator(x):
-        return 0.5 * (mass @ x) - apply_k(x) - eta_c * apply_d(x)
+        return 0.5 * (mass_d @ x) - apply_k(x).to(torch.complex128) - eta_c * apply_d(x)
 
     u_inc, du_inc = incident_trace(wave, mesh, p1c)
     rhs = mass @ u_inc - eta_c * (mass @ du_inc)
     t1 = time.perf_counter()
-    res = gmres(operator, rhs, tol=cfg.tol, restart=cfg.restart, max_iter=cfg.max_iter)
+    res = gmres(operator, torch.from_numpy(np.asarray(rhs, np.complex128)).to(dev), tol=cfg.tol,
+                restart=cfg.restart, max_iter=cfg.max_iter)
+    res = GmresResult(res.x.cpu().numpy(), res.converged, res.iterations, res.residual,
+                      res.residuals, res.restarts)
     t2 = time.perf_counter()
     if not res.converged:
         err = SolverError(f"GMRES did not reach tolerance {cfg.tol:g} within "
@@ -392,3 +415,44 @@ def burton_miller_solve(cfg: ScatterConfig, wave: PlaneWave | None = None, mode:
                        residual=res.residual, residuals=res.residuals,
                        timings={"assembly": t1 - t0, "solve": t2 - t1}, mode=mode,
                        wavenumber=k, n_dofs=p1c.n_dofs, n_elements=len(mesh.elements))
+
+
+def target_strength(u_sct, u0: complex, radius: float):
+    """Bistatic target strength TS = 20 log10(R |u_sct| / |u0|) in dB
+    (scatter.py:411-424): scalars give a float, arrays an array; a silent
+    direction is -inf."""
+    if radius <= 0.0:
+        raise ConfigError(f"radius must be > 0, got {radius}")
+    if u0 == 0:
+        raise ConfigError("reference amplitude u0 must be nonzero")
+    ratio = radius * np.abs(np.asarray(u_sct) / u0)
+    with np.errstate(divide="ignore"):
+        db = 20.0 * np.log10(ratio)
+    return float(db) if np.ndim(u_sct) == 0 else db
+
+
+def deviation(u_a, u_b) -> float:
+    """Mean relative magnitude deviation (1/n) sum ||a_i| - |b_i|| / |b_i| of a
+    far field against a reference one (the paper's Delta_sct,
+    scatter.py:427-441)."""
+    mag_a = np.abs(np.asarray(u_a)).ravel()
+    mag_b = np.abs(np.asarray(u_b)).ravel()
+    if mag_a.shape != mag_b.shape or mag_a.size == 0:
+        raise ConfigError(f"fields must have equal nonzero lengths, got {mag_a.shape} "
+                          f"and {mag_b.shape}")
+    if not mag_b.all():
+        raise ZeroDivisionError(f"reference field vanishes at sample index "
+                                f"{int(np.argmin(mag_b != 0.0))}")
+    return float(np.mean(np.abs(mag_a - mag_b) / mag_b))
+
+
+def write_far_field_csv(path, angles_deg, values, u0: complex, radius: float) -> None:
+    """One CSV row per observation angle: theta_deg, re, im, abs, ts_db
+    (scatter.py:444-452, same header and number formats)."""
+    vals = np.asarray(values)
+    ts = np.atleast_1d(target_strength(vals, u0, radius))
+    rows = ["theta_deg,re,im,abs,ts_db"]
+    rows += [f"{a:.6f},{v.real:.12e},{v.imag:.12e},{abs(v):.12e},{t:.6f}"
+             for a, v, t in zip(angles_deg, vals, ts)]
+    with open(path, "w", encoding="utf-8") as f:
+        f.write("\n".join(rows) + "\n")

@@ -223,3 +223,44 @@ def test_hull_mid_matches_reference(name):
         scale = np.sqrt(np.mean(np.abs(y) ** 2))
         err = np.abs(y[g["rows"]] - g["exact"][t]).max() / scale
         assert abs(err - g["ref_err"][t]) <= 1e-6, (err, g["ref_err"][t])
+
+
+@pytest.mark.parametrize("fam,eq,op,k,prec", [("p0", "laplace", "slp", 0.0, "double"),
+                                              ("p0", "helmholtz", "slp", 4.0, "double"),
+                                              ("p1c", "laplace", "dlp", 0.0, "single")])
+def test_device_matvec_is_bitwise_reproducible(fam, eq, op, k, prec):
+    """No float atomics: repeated device matvecs (host and device-pointer
+    entry points) return identical bits (hmatrix.py:441-446 promise)."""
+    import torch
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix, hmat_matvec
+    v, e, spec, sp, bt = problem(30, fam, eq, op, k, prec)
+    h = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=1e-4))
+    rd = np.dtype(spec.result_dtype)
+    x = np.random.default_rng(9).standard_normal(sp.n_dofs).astype(rd)
+    y1 = hmat_matvec(h, x)
+    y2 = hmat_matvec(h, x)
+    assert np.array_equal(y1, y2)
+    part = h.parts[0][1]
+    tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32,
+           np.dtype(np.complex128): torch.complex128, np.dtype(np.complex64): torch.complex64}[rd]
+    xd = torch.from_numpy(x).to("cuda")
+    yd = torch.empty(sp.n_dofs, dtype=tdt, device="cuda")
+    s = torch.cuda.current_stream()
+    for _ in range(2):
+        part.matvec_device(xd.data_ptr(), yd.data_ptr(), s.cuda_stream)
+        s.synchronize()
+        assert np.array_equal(yd.cpu().numpy(), y1)
+    yh = hmat_matvec(h, x, device=False)
+    assert np.abs(y1 - yh).max() <= (1e-12 if prec == "double" else 1e-5) * np.abs(yh).max()
+
+
+def test_matvec_promotes_like_the_reference():
+    """float32 H-matrix times a float64 vector returns float64
+    (np.result_type(h.dtype, x.dtype), hmatrix.py:455)."""
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix, hmat_matvec
+    v, e, spec, sp, bt = problem(10, "p0", "laplace", "slp", 0.0, "single")
+    h = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=1e-4))
+    x = np.random.default_rng(2).standard_normal(sp.n_dofs)
+    assert hmat_matvec(h, x).dtype == np.float64
+    assert hmat_matvec(h, x.astype(np.complex128)).dtype == np.complex128
+    assert hmat_matvec(h, x.astype(np.float32)).dtype == np.float32
