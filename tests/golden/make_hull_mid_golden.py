@@ -3,7 +3,7 @@
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_hull_mid_golden.py
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_hull_mid_golden.py 90 700
-        (126 000 triangles, ~30 minutes: hull_126k.npz, y stored on 4096 rows)
+        (125 820 triangles, ~20 minutes: hull_125k.npz, y stored on 4096 rows)
 
 Question it answers (VERDICT r01 "C4 accuracy"): is the ≈0.1 sampled-row
 error of the 504k-triangle hull at ACA eps 1e-3 a GPU defect or a property of

@@ -196,15 +196,16 @@ def test_streamed_payloads_equal_deferred_copy(monkeypatch, eq, k, zc):
     ref.close()
 
 
-@pytest.mark.parametrize("name", ["hull_mid", "hull_126k"])
+@pytest.mark.parametrize("name", ["hull_mid", "hull_125k"])
 def test_hull_mid_matches_reference(name):
     """C4 accuracy question (tests/golden/make_hull_mid_golden.py): on 31k- and
     126k-triangle hulls (Helmholtz SLP P0, 8 elements per wavelength, eps 1e-3)
-    the reference's OWN H-matrix misses the exact operator rows by ~9 eps.  The
-    GPU assembly follows the same pivots (its matvec equals the reference's
-    H-matrix matvec to rounding), and therefore reproduces that error — the
-    0.1 sampled-row error of the 504k hull is the reference ACA's behaviour on
-    thin bodies, not a device defect."""
+    the reference's OWN H-matrix misses the exact operator rows by 8e-3..9e-3
+    (31k) and 0.039..0.097 (126k), growing with the mesh like the 0.1 of the
+    504k C4 hull.  The GPU assembly follows the same pivots (its matvec equals
+    the reference's H-matrix matvec to rounding) and therefore reproduces that
+    error: the C4 error is the reference ACA's behaviour on thin bodies at this
+    tolerance, not a device defect."""
     import os
     from conftest import GOLDEN, golden
     from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix
