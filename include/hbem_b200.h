@@ -234,6 +234,10 @@ int hbem_hmat_stats_get(const hbem_hmat *h, hbem_hmat_stats *stats);
    payloads in their arenas (element units), column-major per rank. */
 int hbem_hmat_leaf_meta(const hbem_hmat *h, int32_t *kind, int32_t *rank, int32_t *flags,
                         int64_t *off_u, int64_t *off_v, int64_t *off_dense);
+/* per leaf: the ACA residual indicator of LowRankBlock.residual (hmatrix.py:
+ * 241-268, 377-382: last rank-1 update relative to the accumulated Frobenius
+ * norm; 0 for dense leaves and blocks without terms) */
+int hbem_hmat_leaf_residual(const hbem_hmat *h, double *resid);
 /* D2H of the factor/dense arenas in the result dtype (complex interleaved). */
 int hbem_hmat_copy_arenas(const hbem_hmat *h, void *u, void *v, void *dense);
 /* y = H x in original DOF order; x, y host arrays of the result dtype. */

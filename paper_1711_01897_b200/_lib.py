@@ -138,6 +138,7 @@ SIGNATURES = [
      [C.c_void_p, C.POINTER(HmatDesc), C.c_void_p, C.POINTER(C.c_void_p)]),
     ("hbem_hmat_execute", C.c_int, [C.c_void_p, C.c_void_p]),
     ("hbem_hmat_stats_get", C.c_int, [C.c_void_p, C.POINTER(HmatStats)]),
+    ("hbem_hmat_leaf_residual", C.c_int, [C.c_void_p, c_double_p]),
     ("hbem_hmat_leaf_meta", C.c_int,
      [C.c_void_p, c_int32_p, c_int32_p, c_int32_p, c_int64_p, c_int64_p, c_int64_p]),
     ("hbem_hmat_copy_arenas", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -252,6 +252,7 @@ __global__ void k_mail(MailCopy m) {
 struct LeafMeta {
   int *kind, *rank, *flags;           // L each
   long long *off_u, *off_v, *off_d;   // L each
+  double *resid;                      // L: ACA residual indicator (LowRankBlock.residual)
 };
 
 struct ClsStat {
@@ -277,6 +278,9 @@ __global__ void k_classify(AcaDev S, int na, const int *adm_leaf, const long lon
     M.flags[lf] = (conv ? 1 : 0) | (exh ? 2 : 0);
     M.off_u[lf] = lr ? blk_uoff[q] : -1;
     M.off_v[lf] = lr ? blk_voff[q] : -1;
+    // last update relative to the Frobenius norm (hmatrix.py:377-382); inf
+    // until a term was accepted, 0 for a block without terms
+    M.resid[lf] = k > 0 ? S.resid[q] : 0.0;
     if (lr) M.off_d[lf] = -1;  // dense offsets after the scan
     dsz[q] = make_longlong2(lr ? 0 : h * w, 0);
     flag_lr[q] = lr ? 1 : 0;
@@ -1041,6 +1045,8 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
     HB_CHECK(dalloc(H, &M.off_u, (size_t)std::max<int64_t>(3 * L, 1)));
     M.off_v = M.off_u + L;
     M.off_d = M.off_u + 2 * L;
+    HB_CHECK(dalloc(H, &M.resid, (size_t)std::max<int64_t>(L, 1)));
+    HB_CUDA(cudaMemset(M.resid, 0, (size_t)std::max<int64_t>(L, 1) * 8));
     HB_CUDA(cudaMemset(M.kind, 0, (size_t)3 * L * 4));
     HB_CUDA(cudaMemset(M.off_u, 0xff, (size_t)2 * L * 8));
     HB_CUDA(cudaMemcpy(M.off_d, off_dense0.data(), (size_t)L * 8, cudaMemcpyHostToDevice));
@@ -1737,6 +1743,15 @@ int hbem_hmat_leaf_meta(const hbem_hmat *h, int32_t *kind, int32_t *rank, int32_
   if (off_u) HB_CUDA(cudaMemcpy(off_u, M.off_u, L * 8, cudaMemcpyDeviceToHost));
   if (off_v) HB_CUDA(cudaMemcpy(off_v, M.off_v, L * 8, cudaMemcpyDeviceToHost));
   if (off_dense) HB_CUDA(cudaMemcpy(off_dense, M.off_d, L * 8, cudaMemcpyDeviceToHost));
+  return HBEM_OK;
+}
+
+int hbem_hmat_leaf_residual(const hbem_hmat *h, double *resid) {
+  if (!h || !resid) return set_error(HBEM_ERR_ARG, "null argument");
+  clear_error();
+  HB_CUDA(cudaSetDevice(h->device));
+  if (h->n_leaves > 0)
+    HB_CUDA(cudaMemcpy(resid, h->meta.resid, (size_t)h->n_leaves * 8, cudaMemcpyDeviceToHost));
   return HBEM_OK;
 }
 

@@ -16,6 +16,7 @@ the only data the GPUs share is the geometry each context staged once.
 from __future__ import annotations
 
 import ctypes as C
+import re
 import threading
 from dataclasses import dataclass
 from typing import Sequence
@@ -188,12 +189,14 @@ class _DevicePart:
             self.off_u = np.empty(L, np.int64)
             self.off_v = np.empty(L, np.int64)
             self.off_d = np.empty(L, np.int64)
+            self.resid = np.empty(L, np.float64)
         check(lib.hbem_hmat_leaf_meta(handle, _lib.ptr(self.kind, C.c_int32),
                                       _lib.ptr(self.rank, C.c_int32),
                                       _lib.ptr(self.flags, C.c_int32),
                                       _lib.ptr(self.off_u, C.c_int64),
                                       _lib.ptr(self.off_v, C.c_int64),
                                       _lib.ptr(self.off_d, C.c_int64)))
+        check(lib.hbem_hmat_leaf_residual(handle, _lib.ptr(self.resid, C.c_double)))
         st = _lib.HmatStats()
         check(lib.hbem_hmat_stats_get(handle, C.byref(st)))
         self.stats = {name: getattr(st, name) for name, _ in _lib.HmatStats._fields_}
@@ -236,7 +239,7 @@ class _DevicePart:
             uu = u[self.off_u[q]: self.off_u[q] + h * r].reshape(r, h).T
             vv = v[self.off_v[q]: self.off_v[q] + w * r].reshape(r, w).T
             fl = int(self.flags[q])
-            return LowRankBlock(uu, vv, r, 0.0, bool(fl & 1), bool(fl & 2))
+            return LowRankBlock(uu, vv, r, float(self.resid[q]), bool(fl & 1), bool(fl & 2))
         o = self.off_d[q]
         return DenseBlock(d[o: o + h * w].reshape(h, w))
 
@@ -502,8 +505,14 @@ COUNTER_NAMES = ("host_jobs", "backend_jobs", "singular_pairs", "aca_converged",
 def assemble_hmatrix(spec: OperatorSpec, test_space, trial_space, block_tree: BlockClusterTree,
                      cfg: AcaConfig | None = None, backends: Sequence[GpuBackend] | None = None,
                      assembly_config: AssemblyConfig | None = None,
-                     stats: dict | None = None) -> HMatrix:
-    """hmatrix.py:759-811 on the GPU (see module docstring)."""
+                     stats: dict | None = None, out=None) -> HMatrix:
+    """hmatrix.py:759-811 on the GPU (see module docstring).
+
+    ``out`` (single device): page-locked host arrays (u, v, dense) of the
+    result dtype (``pinned_empty``) that receive the payloads while the
+    assembly runs: converged low-rank factors stream over PCIe wave by wave,
+    dense leaves when the near field completes, so the host copy of the
+    H-matrix is complete when the call returns."""
     cfg = cfg if cfg is not None else AcaConfig()
     acfg = assembly_config if assembly_config is not None else AssemblyConfig()
     if block_tree.shape != (test_space.n_dofs, trial_space.n_dofs):
@@ -521,6 +530,8 @@ def assemble_hmatrix(spec: OperatorSpec, test_space, trial_space, block_tree: Bl
         ictx = make_integration_context(spec, test_space, trial_space, acfg.regular_order,
                                         acfg.singular_base_order)
         dev_ctxs = [init_gpu_device(ictx, 0)]
+    if out is not None and len(dev_ctxs) != 1:
+        raise ConfigError("out= streaming takes one device; pass out per part otherwise")
     splits = split_leaves(block_tree, len(dev_ctxs))
     parts: list = [None] * len(dev_ctxs)
     errors: list = []
@@ -528,7 +539,7 @@ def assemble_hmatrix(spec: OperatorSpec, test_space, trial_space, block_tree: Bl
     def run(i):
         try:
             parts[i] = _assemble_part(dev_ctxs[i], block_tree, splits[i], test_space,
-                                      trial_space, cfg, acfg)
+                                      trial_space, cfg, acfg, out=out)
         except Exception as exc:  # noqa: BLE001 - re-raised in the caller
             errors.append((i, exc))
 
@@ -543,6 +554,11 @@ def assemble_hmatrix(spec: OperatorSpec, test_space, trial_space, block_tree: Bl
     if errors:
         i, exc = errors[0]
         ids = splits[i]
+        # a failure the device attributes to one block is reported like the
+        # reference's assemble_leaf (hmatrix.py:745-751), else by device range
+        blk = re.search(r"block rows \[\d+, \d+\) x cols \[\d+, \d+\)", str(exc))
+        if blk:
+            raise AssemblyError(f"{blk.group(0)} failed: {exc}") from exc
         raise AssemblyError(f"device {i} failed assembling leaves [{ids[0] if len(ids) else 0}, "
                             f"{ids[-1] + 1 if len(ids) else 0}): {exc}") from exc
     part_list = [(splits[i], parts[i]) for i in range(len(parts))]

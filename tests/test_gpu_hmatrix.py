@@ -138,6 +138,13 @@ def test_c1_config_vs_oracle(rng):
     ranks = np.array([p.rank if hasattr(p, "rank") else -1 for p in h.payloads])
     ref_ranks = np.array([p.rank if isinstance(p, O.LowRank) else -1 for p in ref_payloads])
     assert (ranks == ref_ranks).mean() >= 0.95
+    # LowRankBlock.residual (hmatrix.py:241-268): the last update relative to
+    # the accumulated norm, as the reference's aca reports it
+    pairs = [(p.residual, q.residual) for p, q in zip(h.payloads, ref_payloads)
+             if hasattr(p, "rank") and isinstance(q, O.LowRank) and p.rank == q.rank]
+    assert pairs and all(np.isfinite(a) and a > 0 for a, _ in pairs)
+    close = np.mean([abs(a - b) <= 1e-6 * b for a, b in pairs])
+    assert close >= 0.95, close
     assert stats["singular_pairs"] == asm.counters["singular_pairs"]
     cs = compression_stats(h)
     assert cs.ratio < 1.0
@@ -215,3 +222,24 @@ def test_rank_capacity_overflow_retries_with_larger_table():
     assert st_small["capacity_retries"] >= 2 and st_big["capacity_retries"] == 0
     x = np.random.default_rng(5).standard_normal(sp.n_dofs)
     assert np.array_equal(hmat_matvec(h1, x, device=False), hmat_matvec(h2, x, device=False))
+
+
+def test_public_out_streams_payloads_into_host_arenas():
+    """assemble_hmatrix(..., out=(u, v, dense)) fills page-locked host arenas
+    during the assembly; the payloads equal those of a plain assembly."""
+    from paper_1711_01897_b200.hmatrix import AcaConfig, assemble_hmatrix, pinned_empty
+    from paper_1711_01897_b200.meshes import geodesic_sphere
+    v, e = geodesic_sphere(14)
+    spec, sp, bt = setup(v, e, "p0", "laplace", "slp", 0.0)
+    st = {}
+    ref = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=1e-4), stats=st)
+    out = tuple(pinned_empty(st[n] + 8, np.float64)
+                for n in ("u_entries", "v_entries", "dense_entries"))
+    h = assemble_hmatrix(spec, sp, sp, bt, AcaConfig(epsilon=1e-4), out=out)
+    for a, b in zip(ref.payloads, h.payloads):
+        assert type(a) is type(b)
+        if hasattr(a, "u"):
+            assert np.array_equal(a.u, b.u) and np.array_equal(a.v, b.v)
+            assert a.residual == b.residual
+        else:
+            assert np.array_equal(a.a, b.a)
