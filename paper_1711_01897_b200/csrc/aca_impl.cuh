@@ -155,6 +155,7 @@ __global__ void k_jobs(AcaDev S, int n, int col) {
     const long long pe = S.pend[b];
     J.pe = pe >= 0 ? pe : S.pool_base + sc.pool - nd.pool;
     J.nfix = r0 + J.fix;
+    J.mofs = S.cmask_off[b];
     J.vstart = c0;
     J.nvar = J.w;
     J.cur = J.fix;
@@ -164,6 +165,7 @@ __global__ void k_jobs(AcaDev S, int n, int col) {
     J.fix = S.pcol[b];
     J.pe = S.pend[b];
     J.nfix = c0 + J.fix;
+    J.mofs = S.rmask_off[b];
     J.vstart = r0;
     J.nvar = J.h;
     J.cur = S.cur[b];
@@ -282,7 +284,7 @@ struct JobS {
   long long rsc_off;  // element-row values (linear spaces)
   int b, h, w, k, fix, cur;
   unsigned mw;      // used-index mask word of the varying side at this tile
-  int pad_;
+  int nfix;         // tree position of the fixed DOF (its element record, P0)
 };
 
 // ---------------------------------------------------------------------------
@@ -495,7 +497,8 @@ __device__ __forceinline__ bool stage_job(const AcaDev &S, int p, int n, int key
   js.pe = J.pe;
   js.part = J.part;
   js.rsc_off = J.rsc;
-  js.mw = COL ? S.rmask[S.rmask_off[J.b] + t] : S.cmask[S.cmask_off[J.b] + t];
+  js.mw = (COL ? S.rmask : S.cmask)[J.mofs + t];
+  js.nfix = J.nfix;
   js.b = J.b;
   js.h = J.h;
   js.w = J.w;
@@ -582,11 +585,15 @@ __device__ __forceinline__ void fix_from_rec(const ElemRec<T> &r, T c0, T c1, T 
 // NJ fixed elements F against the lane's element (points y, local |y'|^2 in
 // ny, normal nl).  FIXED_TEST: the fixed elements are test elements (row
 // jobs); otherwise trial elements (column jobs).
-template <typename T, bool C, int OP, bool HELM, bool FIXED_TEST, int NJ>
+// NEAR: near-field (inadmissible) pairs, always the direct difference (the
+// local-frame expansion's cancellation bound needs admissibility); the float64
+// single layer still uses the folded rsqrt polynomial (POLY)
+template <typename T, bool C, int OP, bool HELM, bool FIXED_TEST, int NJ, bool NEAR = false>
 __device__ __forceinline__ void p0_quad(const RuleTab<T> &R, const FixRec<T> *const (&F)[NJ],
                                         const T (&y)[18], const T (&ny)[6], const T (&nl)[4],
                                         typename Num<T, C>::V (&out)[NJ]) {
-  constexpr bool LOCAL = P0Local<T, OP>::value;
+  constexpr bool LOCAL = !NEAR && P0Local<T, OP>::value;
+  constexpr bool POLY = P0Local<T, OP>::value;
   T sr[NJ], si[NJ];
 #pragma unroll
   for (int j = 0; j < NJ; ++j) { sr[j] = T(0); si[j] = T(0); }
@@ -602,10 +609,16 @@ __device__ __forceinline__ void p0_quad(const RuleTab<T> &R, const FixRec<T> *co
       const T w = FIXED_TEST ? R.w2[o][i] : R.w2[i][o];
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
-        if constexpr (LOCAL) {
-          const double r2 =
-              fma(f[j][0], y[3 * i], fma(f[j][1], y[3 * i + 1], fma(f[j][2], y[3 * i + 2],
-                                                                    f[j][3] + ny[i])));
+        if constexpr (POLY) {
+          double r2;
+          if constexpr (LOCAL) {
+            r2 = fma(f[j][0], y[3 * i], fma(f[j][1], y[3 * i + 1], fma(f[j][2], y[3 * i + 2],
+                                                                      f[j][3] + ny[i])));
+          } else {
+            const double d0 = f[j][0] - y[3 * i], d1 = f[j][1] - y[3 * i + 1],
+                         d2 = f[j][2] - y[3 * i + 2];
+            r2 = fma(d2, d2, fma(d1, d1, d0 * d0));
+          }
           const double s = rsq_seed(r2);
           const double d = fma(r2, s * s, -5.0 / 3.0);
           const double q = fma(d, d, 20.0 / 9.0);
@@ -635,7 +648,7 @@ __device__ __forceinline__ void p0_quad(const RuleTab<T> &R, const FixRec<T> *co
   }
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
-    const T scale = (F[j]->n[3] * nl[3]) * T(LOCAL ? 0.375 * kInv4Pi : kInv4Pi);
+    const T scale = (F[j]->n[3] * nl[3]) * T(POLY ? 0.375 * kInv4Pi : kInv4Pi);
     out[j] = Num<T, C>::mk(scale * sr[j], HELM ? scale * si[j] : T(0));
   }
 }
@@ -719,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_P0_MINB) k_aca_p0(Prob<T> P, 
         sout[wid][lane] = pool + js.pe + (COL ? 0 : js.h) + t * 32;
         srec[wid][lane] = S.part + js.part + (long long)t * part_len(js.k, NC);
         ElemRec<T> r;
-        load_rec<T>(COL ? P.srec : P.trec, (COL ? S.c0[js.b] : S.r0[js.b]) + js.fix, r);
+        load_rec<T>(COL ? P.srec : P.trec, js.nfix, r);
         FixRec<T> f;
         fix_from_rec<T, LOCAL>(r, c0, c1, c2, f);
         sr[wid][lane] = f;

@@ -422,6 +422,7 @@ struct Job {
   long long pe;     // pool record of the pending term [u (h) | v (w)]
   long long part;   // first partial record of this job (doubles)
   long long rsc;    // linear spaces: element-row values of this job (V units)
+  long long mofs;   // used-index mask words of the varying side (rmask / cmask offset)
 };
 
 // partial record per (job, 32-wide tile): best |val| over unmasked entries,

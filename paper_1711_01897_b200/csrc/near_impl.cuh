@@ -10,7 +10,7 @@
 #pragma once
 #include <algorithm>
 
-#include "hmat_common.cuh"
+#include "aca_impl.cuh"
 
 namespace hb {
 
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_near_p0(Prob<T> P, De
   using N = Num<T, C>;
   using V = typename N::V;
   constexpr unsigned kAll = 0xffffffffu;
-  __shared__ ElemRec<T> sr[kWarps][32];
+  __shared__ FixRec<T> sr[kWarps][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long item = (long long)blockIdx.x * kWarps + wid;
   if (item >= D.n_items) return;
@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_near_p0(Prob<T> P, De
   const bool valid = c < w;
   ElemRec<T> my;
   load_rec<T>(P.srec, c0 + (valid ? c : w - 1), my);
+  T ny[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
   V *out = static_cast<V *>(D.out) + D.off[s];
   unsigned long long nsing = 0;
   for (int seg = 0; seg < h; seg += 32) {
@@ -57,19 +58,21 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_near_p0(Prob<T> P, De
     if (lane < nseg) {
       ElemRec<T> r;
       load_rec<T>(P.trec, r0 + seg + lane, r);
-      sr[wid][lane] = r;
+      FixRec<T> f;
+      fix_from_rec<T, false>(r, T(0), T(0), T(0), f);
+      sr[wid][lane] = f;
     }
     __syncwarp();
     for (int i = 0; i < nseg; i += 2) {
       const int nj = i + 1 < nseg ? 2 : 1;
       V val[2];
       if (nj == 2) {
-        const ElemRec<T> *const F2[2] = {&sr[wid][i], &sr[wid][i + 1]};
-        p0_pairs_fx<T, C, OP, HELM, true, 2>(P.R, F2, my.q, my.n, val);
+        const FixRec<T> *const F2[2] = {&sr[wid][i], &sr[wid][i + 1]};
+        p0_quad<T, C, OP, HELM, true, 2, true>(P.R, F2, my.q, ny, my.n, val);
       } else {
-        const ElemRec<T> *const F1[1] = {&sr[wid][i]};
+        const FixRec<T> *const F1[1] = {&sr[wid][i]};
         V v1[1];
-        p0_pairs_fx<T, C, OP, HELM, true, 1>(P.R, F1, my.q, my.n, v1);
+        p0_quad<T, C, OP, HELM, true, 1, true>(P.R, F1, my.q, ny, my.n, v1);
         val[0] = v1[0];
       }
 #pragma unroll
