@@ -553,11 +553,6 @@ template <typename T, int OP> struct P0Local {
   static constexpr bool value = std::is_same<T, double>::value && OP == HBEM_SLP;
 };
 
-__device__ __forceinline__ double rsq_seed(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  return y;
-}
 
 template <typename T, bool LOCAL>
 __device__ __forceinline__ void fix_from_rec(const ElemRec<T> &r, T c0, T c1, T c2,
