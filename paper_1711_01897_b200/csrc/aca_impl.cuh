@@ -1042,6 +1042,37 @@ __device__ __forceinline__ double group_sum(double v) {
   return v;
 }
 
+// sums over a job's tiles of its first kk dots (re, im): group lanes over
+// the tiles (t = sl, sl + 8, ...), all kk dots per tile, then the butterfly,
+// which leaves every lane with all kk sums; a long row costs ntiles / 8
+// iterations of independent loads, not a serial chain over its tiles
+template <bool C>
+__device__ __forceinline__ void group_tile_dots(const double *dots, int ntiles, long long stride,
+                                                int kk, int sl, double (&sr)[kFinRegs],
+                                                double (&si)[kFinRegs]) {
+  constexpr int NC = C ? 2 : 1;
+#pragma unroll
+  for (int l = 0; l < kFinRegs; ++l) { sr[l] = 0.0; si[l] = 0.0; }
+  if (dots) {
+    for (int t = sl; t < ntiles; t += kFinLanes) {
+      const double *r = dots + t * stride;
+#pragma unroll
+      for (int l = 0; l < kFinRegs; ++l)
+        if (l < kk) {
+          sr[l] += r[l * NC];
+          if (C) si[l] += r[l * NC + 1];
+        }
+    }
+  }
+#pragma unroll
+  for (int o = kFinLanes / 2; o > 0; o >>= 1)
+#pragma unroll
+    for (int l = 0; l < kFinRegs; ++l) {
+      sr[l] += __shfl_xor_sync(kFull, sr[l], o);
+      if (C) si[l] += __shfl_xor_sync(kFull, si[l], o);
+    }
+}
+
 // pivot statistics of a job's residual row / column from its tile records
 // (aca_epi): group lanes over the tiles in order, then the butterfly; argmax
 // over unused indices with the first index on ties, sum |val|^2
@@ -1078,19 +1109,18 @@ __global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int n) {
   int bidx;
   const long long ps = part_len(J.k, N::NC);
   tile_stats(act ? S.part + J.part : nullptr, tiles_of(J.w), ps, sl, best, bidx, ss);
-  if (act && sl < min(J.k, kFinRegs)) {
-    // this row's dots with the first terms, summed over its tiles in order,
-    // for the column finalize's cross terms (compact, indexed by block)
-    const double *rd = S.part + J.part + 4 + sl * N::NC;
-    const int ntr = tiles_of(J.w);
-    double sr = 0.0, si = 0.0;
-    for (int t = 0; t < ntr; ++t) {
-      sr += rd[t * ps];
-      if (C) si += rd[t * ps + 1];
+  {
+    // this row's dots with the first terms, summed over its tiles (group
+    // lanes over the tiles, then the butterfly; fixed order) for the column
+    // finalize's cross terms (compact, indexed by block)
+    const int kk = act ? min(J.k, kFinRegs) : 0;
+    double sr[kFinRegs], si[kFinRegs];
+    group_tile_dots<C>(act ? S.part + J.part + 4 : nullptr, tiles_of(J.w), ps, kk, sl, sr, si);
+    if (act && sl < kk) {
+      double *o = S.rsum + (long long)J.b * (kFinRegs * 2) + sl * 2;
+      o[0] = sr[sl];
+      o[1] = si[sl];
     }
-    double *o = S.rsum + (long long)J.b * (kFinRegs * 2) + sl * 2;
-    o[0] = sr;
-    o[1] = si;
   }
   if (!act || sl != 0) return;
   const int b = J.b, h = J.h, w = J.w, i = J.fix;
@@ -1153,22 +1183,30 @@ __global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
   // vdot(v_l, v) = vdot(r_l, r) / (conj(p_l) p); lane sl sums the dots of
   // terms sl, sl + 8, ... over the column and row tiles in tile order
   double cross = 0.0;
-  if (act && !small) {
+  // column dots of the first terms, summed over the column tiles (all lanes)
+  const bool need = act && !small;
+  double csr[kFinRegs], csi[kFinRegs];
+  group_tile_dots<C>(need ? crec + 4 : nullptr, ntc, ps, need ? min(k, kFinRegs) : 0, sl, csr,
+                     csi);
+  if (need) {
     const V *pool = static_cast<const V *>(S.pool);
     const double *cd = crec + 4;
     const double *rd = S.rpart + S.rowpart[b] + 4;
     const long long *tl = S.terms + (long long)b * S.tmax;
     for (int l = sl; l < k; l += kFinLanes) {
       double ur = 0.0, ui = 0.0, vr = 0.0, vi = 0.0;
-      for (int t = 0; t < ntc; ++t) {
-        ur += cd[t * ps + (long long)l * NC];
-        if (C) ui += cd[t * ps + (long long)l * NC + 1];
-      }
       if (l < kFinRegs) {
+#pragma unroll
+        for (int q = 0; q < kFinRegs; ++q)
+          if (q == l) { ur = csr[q]; ui = csi[q]; }
         const double *o = S.rsum + (long long)b * (kFinRegs * 2) + l * 2;
         vr = o[0];
         vi = o[1];
-      } else {
+      } else {  // terms beyond the register batch: serial over the tiles
+        for (int t = 0; t < ntc; ++t) {
+          ur += cd[t * ps + (long long)l * NC];
+          if (C) ui += cd[t * ps + (long long)l * NC + 1];
+        }
         for (int t = 0; t < ntr; ++t) {
           vr += rd[t * ps + (long long)l * NC];
           if (C) vi += rd[t * ps + (long long)l * NC + 1];
