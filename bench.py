@@ -57,8 +57,8 @@ DP_INSTR_PER_PAIR = 12 * 36 + 2
 def _ncu_traffic():
     """DRAM bytes per k_aca_p0 launch (dram__bytes_read.sum + dram__bytes_write.sum,
     averaged over the 30 launches of one C5 FP64 assembly) from the committed ncu
-    capture profiles/r01_traffic_k_aca_p0.json; None when absent."""
-    p = os.path.join(ROOT, "profiles", "r01_traffic_k_aca_p0.json")
+    capture profiles/r02_traffic_k_aca_p0.json; None when absent."""
+    p = os.path.join(ROOT, "profiles", "r02_traffic_k_aca_p0.json")
     try:
         with open(p) as f:
             return float(json.load(f)["dram_bytes_per_launch"])

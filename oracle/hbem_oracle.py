@@ -655,6 +655,10 @@ class Assembler:
         self.cinv[cols.permutation] = np.arange(len(cols.permutation))
         self.counters = {"regular_pairs": 0, "singular_pairs": 0, "aca_fallback_dense": 0,
                          "dense_leaves": 0, "lowrank_leaves": 0}
+        # optional batched integrator for the regular pairs, the reference's
+        # backend routing with threshold 1 (hmatrix.py:608-613): a callable
+        # pairs -> (re, im) supplied by a test (e.g. a GPU backend)
+        self.regular_fn = None
 
     @staticmethod
     def _of(inc, d):
@@ -678,7 +682,8 @@ class Assembler:
         touch = (ea[:, :, None] == eb[:, None, :]).any(axis=(1, 2))
         reg = np.nonzero(~touch)[0]
         if len(reg):
-            re, im = integrate_batch(P, pairs[reg])
+            re, im = (integrate_batch(P, pairs[reg]) if self.regular_fn is None
+                      else self.regular_fn(pairs[reg]))
             out[reg] = re if im is None else re + 1j * im
             self.counters["regular_pairs"] += len(reg)
         for p in np.nonzero(touch)[0]:

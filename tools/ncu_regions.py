@@ -13,7 +13,7 @@ def main():
     reasons = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
     ri = [h.index(c) for c in reasons]
     rows = [(r[src].strip(), int(r[ex] or 0), [int(r[i] or 0) for i in ri]) for r in k["rows"]]
-    mufu = [i for i, (s, n, _) in enumerate(rows) if "MUFU.RSQ64H" in s and n > 0]
+    mufu = [i for i, (s, n, _) in enumerate(rows) if "MUFU.RSQ" in s and n > 0]
     a, b = mufu[0], mufu[-1]
     jobs = max(n for _, n, _ in rows[a:b])
     tot = sum(sum(v) for _, _, v in rows)
