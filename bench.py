@@ -49,9 +49,10 @@ UNIT = "element-pair integrals/s"
 # 36 quadrature-point pairs x (diff 3 + r^2 5 + accumulate 2) = 360 FLOP
 # (+ 36 rsqrt, not counted as FLOP)
 FLOP_PER_PAIR_LAP_SLP_P0 = 360
-# issued FP64 instructions per regular pair in k_aca_p0 (SASS: 3 DADD, DMUL + 2 DFMA,
-# MUFU.RSQ64H + 5 refinement, 1 accumulate per quadrature-point pair) + 2 epilogue
-DP_INSTR_PER_PAIR = 12 * 36 + 2
+# issued FP64 instructions per regular pair in k_aca_p0's quadrature (SASS, round 2:
+# local-frame r^2 = 1 DADD + 3 DFMA, folded rsqrt polynomial DMUL + 2 DFMA, weight
+# DMUL + accumulate DFMA = 9 per quadrature-point pair, + 1 MUFU.RSQ64H) + 2 scale
+DP_INSTR_PER_PAIR = 9 * 36 + 2
 
 
 def _ncu_traffic():
@@ -404,7 +405,7 @@ def run_ours(args):
                 # the SASS instruction count is the FP64 kernel's
                 "issue_frac": (dp_issue / (peak.value / 2)
                                if peak.value and args.precision == "double" else None),
-                "issue_model": (f"{DP_INSTR_PER_PAIR} FP64 instructions per pair (12 per "
+                "issue_model": (f"{DP_INSTR_PER_PAIR} FP64 instructions per pair (9 per "
                                 "quadrature-point pair, from cuobjdump -sass) / FP64 lane rate"
                                 if args.precision == "double" else None),
                 "launches_per_step": int_launches // max(args.steps, 1),
