@@ -56,10 +56,6 @@ __global__ void k_mv_dense(int nl, const int *r0, const int *c0, const int *h, c
   if (lane == 0) static_cast<V *>(part)[g] = acc;  // slot: leaf row g of this list
 }
 
-// one warp per low-rank block: s_l = v_l . x, y += sum_l u_l s_l.  The term
-// offsets and pivots are fetched lane-parallel (lane l holds term l) and
-// broadcast by shuffles, so every factor load is independent of the others
-// (no per-term dependent global load); dots run four terms at a time.
 template <typename T, bool C>
 __device__ __forceinline__ typename Num<T, C>::V shfl_v(typename Num<T, C>::V v, int src) {
   if constexpr (C) {
@@ -70,6 +66,43 @@ __device__ __forceinline__ typename Num<T, C>::V shfl_v(typename Num<T, C>::V v,
     return __shfl_sync(0xffffffffu, v, src);
   }
 }
+
+// one warp per dense leaf (near field: at most 32 x 32): lane r owns row r and
+// streams it (each row's 32 values are one 256-byte run, so every DRAM sector
+// is used once through L1), x of the leaf's columns is broadcast by shuffles;
+// no per-row warp reduction and no leaf search.  The sum order per row is the
+// column order, fixed.
+template <typename T, bool C>
+__global__ void k_mv_dense_leaf(int nl, const int *c0, const int *h, const int *w,
+                                const long long *off, const long long *rowbase,
+                                const void *arena, const void *xt, void *part) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  const long long s = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nl) return;
+  const int hh = h[s], ww = w[s];
+  const V *A = static_cast<const V *>(arena) + off[s];
+  const V *x = static_cast<const V *>(xt) + c0[s];
+  V *out = static_cast<V *>(part) + rowbase[s];
+  for (int r0 = 0; r0 < hh; r0 += 32) {
+    const int r = r0 + lane;
+    const V *row = A + (long long)(r < hh ? r : 0) * ww;
+    V acc = N::zero();
+    for (int c0_ = 0; c0_ < ww; c0_ += 32) {
+      const V xv = c0_ + lane < ww ? x[c0_ + lane] : N::zero();
+      const int cn = min(32, ww - c0_);
+#pragma unroll 8
+      for (int c = 0; c < cn; ++c) acc = N::fma_acc(acc, row[c0_ + c], shfl_v<T, C>(xv, c));
+    }
+    if (r < hh) out[r] = acc;
+  }
+}
+
+// one warp per low-rank block: s_l = v_l . x, y += sum_l u_l s_l.  The term
+// offsets and pivots are fetched lane-parallel (lane l holds term l) and
+// broadcast by shuffles, so every factor load is independent of the others
+// (no per-term dependent global load); dots run four terms at a time.
 
 // low-rank blocks in two passes over (block, chunk) work items:
 //   dots: warp per (block, <= kMvChunk columns): s_l += v_l[chunk] . x[chunk]
@@ -205,10 +238,16 @@ int matvec_launch(const MatvecArgs &M, const AcaDev &S, cudaStream_t st) {
   for (int a = 0; a < 2; ++a) {
     const MatvecArgs::Dense &D = M.dense[a];
     if (D.n <= 0 || D.nrows <= 0) continue;
-    const long long warps = D.nrows;
-    k_mv_dense<T, C><<<(unsigned)((warps + 3) / 4), 128, 0, st>>>(
-        D.n, D.r0, D.c0, D.h, D.w, D.off, D.rowbase, D.nrows, D.arena, M.xt,
-        static_cast<V *>(M.part) + D.part_base);
+    if (a == 0) {  // near-field leaves: warp per leaf, lane per row
+      k_mv_dense_leaf<T, C><<<(unsigned)((D.n + 3) / 4), 128, 0, st>>>(
+          D.n, D.c0, D.h, D.w, D.off, D.rowbase, D.arena, M.xt,
+          static_cast<V *>(M.part) + D.part_base);
+    } else {  // admissible blocks stored densely (any width): warp per row
+      const long long warps = D.nrows;
+      k_mv_dense<T, C><<<(unsigned)((warps + 3) / 4), 128, 0, st>>>(
+          D.n, D.r0, D.c0, D.h, D.w, D.off, D.rowbase, D.nrows, D.arena, M.xt,
+          static_cast<V *>(M.part) + D.part_base);
+    }
   }
   if (M.n_lowrank > 0) {
     k_mv_dots<T, C><<<(unsigned)((M.n_ditems + 3) / 4), 128, 0, st>>>(
