@@ -1001,6 +1001,9 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
         HB_CHECK(restrict_sing_pairs(tab, H->rperm, dci, H->nf_rowbase, nd, H->nf_rows, D.r0,
                                      D.c0, D.w, H->dev_allocs, 0));
       }
+      if (H->p0 && sym) HB_CHECK(sort_sing_pairs(tab, ctx->elem, H->dev_allocs, 0));
+      D.skind[0] = 0;
+      for (int c = 1; c < 4; ++c) D.skind[c] = D.skind[c - 1] + tab.kind_n[c];
       H->sing_pairs_table = tab.n_pairs;
       D.nb_ptr = tab.nb_ptr;
       D.nb_idx = tab.nb_idx;

@@ -509,6 +509,7 @@ struct DenseDev {
   void *stab;
   const int4 *spairs;  // (test e, trial f, slot of (e,f), slot of (f,e) or -1)
   long long n_spairs;
+  long long skind[4];  // sorted by touching class: pairs of class c at [skind[c-1], skind[c])
 };
 
 // P0 singular-table construction (setup) and evaluation (execute)
@@ -516,6 +517,7 @@ struct SingTable {
   int *nb_ptr = nullptr, *nb_idx = nullptr;
   int4 *pairs = nullptr;
   long long nnz = 0, n_pairs = 0;
+  long long kind_n[4] = {0, 0, 0, 0};  // pairs per touching class after sort_sing_pairs
 };
 int build_sing_table(const int4 *d_elem, int m, int nv, bool symmetric, SingTable &out,
                      std::vector<void *> &allocs, cudaStream_t st);
@@ -523,6 +525,10 @@ int build_sing_table(const int4 *d_elem, int m, int nv, bool symmetric, SingTabl
 // (P0: row element in the leaf's row cluster, trial element in its column
 // cluster), so a rank assembling a slice of the leaves integrates only its
 // share of the Sauter-Schwab table
+// order the pairs by touching class (vertex, edge, identical; stable), so a
+// warp's 32 pairs share one Sauter-Schwab rule (lane-per-pair table kernel)
+int sort_sing_pairs(SingTable &tab, const int4 *d_elem, std::vector<void *> &allocs,
+                    cudaStream_t st);
 int restrict_sing_pairs(SingTable &tab, const int *rperm, const int *cinv,
                         const long long *rowbase, int nd, long long nrows, const int *r0,
                         const int *c0, const int *w, std::vector<void *> &allocs,

@@ -107,6 +107,14 @@ __global__ void __launch_bounds__(kThreads, HB_ACA_MINB) k_near_p0(Prob<T> P, De
 // (S = S^T, kernels.py:340-344), so it is also stored at (f, e) and each
 // unordered pair is integrated once.
 // ---------------------------------------------------------------------------
+#ifndef HB_SING_LANES
+#define HB_SING_LANES 1
+#endif
+#ifndef HB_SING_PPW
+#define HB_SING_PPW 8
+#endif
+constexpr int kSingPerWarp = HB_SING_PPW;
+
 template <typename T, bool C, int OP, bool HELM, int NT, int NS>
 __global__ void __launch_bounds__(kThreads) k_sing_table(Prob<T> P, DenseDev D) {
   using N = Num<T, C>;
@@ -134,15 +142,56 @@ __global__ void __launch_bounds__(kThreads) k_sing_table(Prob<T> P, DenseDev D) 
   }
 }
 
+// Singular table, single layer on P0 (the C1/C3/C5 near field): one lane per
+// touching pair, the pairs of one launch all of one touching class (sorted at
+// setup, sort_sing_pairs), so every lane walks the same Sauter-Schwab rule and
+// the rule loads are warp-uniform broadcasts; no cross-lane reduction.  The
+// single layer is symmetric, so the pair is integrated in its canonical
+// orientation (lower element index as test, kernels.py:340-344) and stored
+// at both slots.
+template <typename T, bool C, bool HELM>
+__global__ void __launch_bounds__(kThreads) k_sing_lanes(Prob<T> P, DenseDev D, long long q0,
+                                                         long long q1) {
+  using N = Num<T, C>;
+  using V = typename N::V;
+  const long long q = q0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool act = q < q1;
+  const int4 pr = D.spairs[act ? q : q0];  // idle lanes repeat a pair of the same class
+  const int a = min(pr.x, pr.y), b = max(pr.x, pr.y);
+  const int4 ea = P.G64.elem[a], eb = P.G64.elem[b];
+  const int ta[3] = {ea.x, ea.y, ea.z}, tb[3] = {eb.x, eb.y, eb.z};
+  int pa[3], pb[3];
+  const int kind = classify_pair(ta, tb, pa, pb);
+  double re[1][1], im[1][1];
+  singular_pair_warp<HBEM_SLP, HELM, 1, 1, 1>(P.G64, a, b, kind, pa, pb, re, im);
+  if (!act) return;
+  const V v = N::mk((T)re[0][0], (T)im[0][0]);
+  V *tab = static_cast<V *>(D.stab);
+  tab[pr.z] = v;
+  if (pr.w >= 0) tab[pr.w] = v;
+}
+
 template <typename T, bool C>
 int sing_table_launch(const Prob<T> &P, const DenseDev &D, int op, bool helm, int nt, int ns,
                       cudaStream_t st) {
   if (D.n_spairs <= 0) return HBEM_OK;
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);  // the context's device (set by the caller)
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid =
-      (unsigned)std::min<long long>((D.n_spairs + kWarps - 1) / kWarps, (long long)sms * 16);
+  // short-lived CTAs (kSingPerWarp pairs per warp): the table runs on the
+  // low-priority stream and must hand SM slots back to the ACA phases within
+  // tens of microseconds, not hold them for the whole table
+  const long long per_cta = (long long)kWarps * kSingPerWarp;
+  const unsigned grid = (unsigned)std::min<long long>((D.n_spairs + per_cta - 1) / per_cta, 0x7fffffffll);
+  if (op == HBEM_SLP && nt == 1 && ns == 1 && D.skind[3] == D.n_spairs && HB_SING_LANES) {
+    // pairs sorted by touching class: one launch per class
+    for (int c = 1; c < 4; ++c) {
+      const long long q0 = D.skind[c - 1], q1 = D.skind[c];
+      if (q1 <= q0) continue;
+      const unsigned g = (unsigned)((q1 - q0 + kThreads - 1) / kThreads);
+      if (helm != C) return set_error(HBEM_ERR_KERNEL, "value type does not match the equation");
+      k_sing_lanes<T, C, C><<<g, kThreads, 0, st>>>(P, D, q0, q1);
+      HB_CUDA(cudaGetLastError());
+    }
+    return HBEM_OK;
+  }
   return dispatch_op(op, helm, nt, ns, [&](auto OPc, auto Hc, auto NTc, auto NSc) -> int {
     constexpr int OP = decltype(OPc)::value;
     constexpr bool HH = decltype(Hc)::value != 0;

@@ -111,6 +111,22 @@ __global__ void k_pair_fill(int m, const int *ptr, const int *idx, int sym, cons
   }
 }
 
+// touching class of a pair = number of shared vertex indices (1 vertex, 2
+// edge, 3 identical: classify_pair's kinds, quadrature.py:155-181)
+__global__ void k_pair_kind(const int4 *elem, const int4 *pairs, long long n,
+                            unsigned char *key, unsigned long long *cnt) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int4 pr = pairs[q];
+  const int4 a = elem[pr.x], b = elem[pr.y];
+  const int ta[3] = {a.x, a.y, a.z};
+  int ns = 0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) ns += (ta[i] == b.x || ta[i] == b.y || ta[i] == b.z) ? 1 : 0;
+  key[q] = (unsigned char)ns;
+  atomicAdd(cnt + ns, 1ull);
+}
+
 template <typename X> int alloc(std::vector<void *> &allocs, X **p, size_t n) {
   void *q = nullptr;
   cudaError_t err = cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(X));
@@ -205,6 +221,38 @@ int restrict_sing_pairs(SingTable &tab, const int *rperm, const int *cinv,
   HB_CUDA(e);
   tab.pairs = kept;
   tab.n_pairs = h;
+  return HBEM_OK;
+}
+
+int sort_sing_pairs(SingTable &tab, const int4 *d_elem, std::vector<void *> &allocs,
+                    cudaStream_t st) {
+  for (long long &c : tab.kind_n) c = 0;
+  if (tab.n_pairs <= 0) return HBEM_OK;
+  const long long n = tab.n_pairs;
+  unsigned char *key = nullptr, *key2 = nullptr;
+  unsigned long long *cnt = nullptr;
+  HB_CUDA(cudaMalloc(&key, (size_t)n));
+  HB_CUDA(cudaMalloc(&key2, (size_t)n));
+  HB_CUDA(cudaMalloc(&cnt, 4 * sizeof(unsigned long long)));
+  auto cleanup = [&]() { cudaFree(key); cudaFree(key2); cudaFree(cnt); };
+  HB_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), st));
+  k_pair_kind<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_elem, tab.pairs, n, key, cnt);
+  int4 *sorted = nullptr;
+  HB_CHECK(alloc(allocs, &sorted, (size_t)n));
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, tab.pairs, sorted, n, 0, 2, st);
+  void *tmp = nullptr;
+  HB_CUDA(cudaMalloc(&tmp, std::max<size_t>(tb, 1)));
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tb, key, key2, tab.pairs, sorted, n, 0, 2, st);
+  unsigned long long h[4] = {0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(tmp);
+  cleanup();
+  HB_CUDA(e);
+  if (h[0] != 0) return set_error(HBEM_ERR_KERNEL, "singular table holds a non-touching pair");
+  for (int k = 0; k < 4; ++k) tab.kind_n[k] = (long long)h[k];
+  tab.pairs = sorted;
   return HBEM_OK;
 }
 
