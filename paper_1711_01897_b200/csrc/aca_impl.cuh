@@ -656,23 +656,30 @@ __device__ __forceinline__ void p0_quad(const RuleTab<T> &R, const FixRec<T> *co
 // values of a job are loaded (cp.async) before its integral so their latency
 // hides behind the quadrature.
 // ---------------------------------------------------------------------------
+// warps per CTA of k_aca_p0: independent warps (their items differ in length)
+// so a CTA's slot frees as soon as its own warps finish
+#ifndef HB_ACA_WPC
+#define HB_ACA_WPC 1
+#endif
+constexpr int kP0Warps = HB_ACA_WPC;
+
 template <typename T, bool C, int OP, bool HELM, bool COL>
-__global__ void __launch_bounds__(kThreads, HB_ACA_P0_MINB) k_aca_p0(Prob<T> P, AcaDev S, int n,
+__global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) k_aca_p0(Prob<T> P, AcaDev S, int n,
                                                                    long long n_items) {
   using N = Num<T, C>;
   using V = typename N::V;
   constexpr int NC = N::NC;
   constexpr bool LOCAL = P0Local<T, OP>::value;
   constexpr int kSeg = sizeof(V) > 8 ? 8 : 16;  // jobs staged per segment
-  __shared__ FixRec<T> sr[kWarps][kSeg];
-  __shared__ JobS sj[kWarps][kSeg];
-  __shared__ const V *sfp[kWarps][kSeg][kFinRegs];  // factor values of this tile, term l
-  __shared__ V sjc[kWarps][kSeg][kFinRegs];         // residual coefficients
-  __shared__ V *sout[kWarps][kSeg];                 // this tile of the pending record
-  __shared__ double *srec[kWarps][kSeg];            // this tile's record
-  __shared__ double sred[kWarps][32 * kRedStride];  // transpose scratch
+  __shared__ FixRec<T> sr[kP0Warps][kSeg];
+  __shared__ JobS sj[kP0Warps][kSeg];
+  __shared__ const V *sfp[kP0Warps][kSeg][kFinRegs];  // factor values of this tile, term l
+  __shared__ V sjc[kP0Warps][kSeg][kFinRegs];         // residual coefficients
+  __shared__ V *sout[kP0Warps][kSeg];                 // this tile of the pending record
+  __shared__ double *srec[kP0Warps][kSeg];            // this tile's record
+  __shared__ double sred[kP0Warps][32 * kRedStride];  // transpose scratch
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const long long item = (long long)blockIdx.x * kWarps + wid;
+  const long long item = (long long)blockIdx.x * kP0Warps + wid;
   if (item >= n_items) return;
   const int2 it = S.items[item];
   const int p0 = it.x, t = it.y;
@@ -1352,6 +1359,7 @@ int aca_phase(const Prob<T> &P, AcaDev &S, const PhaseArgs &A, int op, bool helm
   }
   if (n_items > 0) {
     const unsigned grid = (unsigned)((n_items + kWarps - 1) / kWarps);
+    const unsigned grid_p0 = (unsigned)((n_items + kP0Warps - 1) / kP0Warps);
     if (A.int_beg) HB_CUDA(cudaEventRecord(A.int_beg, st));
     int rc = dispatch_op(op, helm, nt, ns, [&](auto OPc, auto Hc, auto NTc, auto NSc) -> int {
       constexpr int OP = decltype(OPc)::value;
@@ -1359,8 +1367,8 @@ int aca_phase(const Prob<T> &P, AcaDev &S, const PhaseArgs &A, int op, bool helm
       constexpr int NT = decltype(NTc)::value, NS = decltype(NSc)::value;
       if constexpr (HH == C) {
         if constexpr (NT == 1 && NS == 1) {
-          if (col) k_aca_p0<T, C, OP, HH, true><<<grid, kThreads, 0, st>>>(P, S, n, n_items);
-          else k_aca_p0<T, C, OP, HH, false><<<grid, kThreads, 0, st>>>(P, S, n, n_items);
+          if (col) k_aca_p0<T, C, OP, HH, true><<<grid_p0, kP0Warps * 32, 0, st>>>(P, S, n, n_items);
+          else k_aca_p0<T, C, OP, HH, false><<<grid_p0, kP0Warps * 32, 0, st>>>(P, S, n, n_items);
         } else {
           if (col)
             k_aca_gen<T, C, OP, HH, NT, NS, true><<<grid, kThreads, 0, st>>>(P, S, n, n_items);
