@@ -32,7 +32,6 @@
 namespace hb {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kNeedThreads = 256;  // k_need block size (block-scan width)
 #ifndef HB_ACA_P0_MINB
 #define HB_ACA_P0_MINB 3  // k_aca_p0 resident CTAs per SM (register cap 168)
 #endif
@@ -77,6 +76,11 @@ __global__ void __launch_bounds__(kNeedThreads) k_need(AcaDev S, int na, int col
                                                       Need *bsum) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = *S.nlist;
+  if ((long long)blockIdx.x * kNeedThreads >= n) {
+    // past the selected list (later waves: most of the blocks)
+    if (threadIdx.x == 0) bsum[blockIdx.x] = Need{0, 0, 0, 0, 0};
+    return;
+  }
   Need d{0, 0, 0, 0, 0};
   if (p < n && p < na) {
     const int b = S.list[p];
@@ -112,25 +116,28 @@ __global__ void __launch_bounds__(kNeedThreads) k_need(AcaDev S, int na, int col
   if (threadIdx.x == kNeedThreads - 1) bsum[blockIdx.x] = inc;
 }
 
-// exclusive scan of the block totals, one CTA (in place)
-static __global__ void __launch_bounds__(1024) k_need_blocks(Need *bsum, int nb) {
+// exclusive scan of the block totals of the selected list, one CTA (in
+// place); the grand total goes to bsum[nb] (the phase's one host read)
+static __global__ void __launch_bounds__(1024) k_need_blocks(Need *bsum, int nb, const int *nlist) {
   using BS = cub::BlockScan<Need, 1024>;
   __shared__ typename BS::TempStorage ts;
   Need carry{0, 0, 0, 0, 0};
-  for (int base = 0; base < nb; base += 1024) {
+  const int nbe = min(nb, (*nlist + kNeedThreads - 1) / kNeedThreads);
+  for (int base = 0; base < nbe; base += 1024) {
     const int i = base + threadIdx.x;
     Need v = i < nb ? bsum[i] : Need{0, 0, 0, 0, 0};
     Need ex, tot;
     BS(ts).ExclusiveScan(v, ex, Need{0, 0, 0, 0, 0}, SumNeed(), tot);
     __syncthreads();
-    if (i < nb) bsum[i] = SumNeed()(carry, ex);
+    if (i < nbe) bsum[i] = SumNeed()(carry, ex);
     carry = SumNeed()(carry, tot);
   }
+  if (threadIdx.x == 0) bsum[nb] = carry;
 }
 
 static __global__ void k_need_carry(AcaDev S, int na, const Need *bsum) {
   const int p = (blockIdx.x + 1) * kNeedThreads + threadIdx.x;
-  if (p < na) S.scan[p] = SumNeed()(bsum[blockIdx.x + 1], S.scan[p]);
+  if (p < na && p < *S.nlist) S.scan[p] = SumNeed()(bsum[blockIdx.x + 1], S.scan[p]);
 }
 
 template <typename T, bool C>
@@ -1032,6 +1039,9 @@ __global__ void __launch_bounds__(kThreads) k_aca_gen(Prob<T> P, AcaDev S, int n
 // (statistics) and its terms (cross-term dots) in one pass; the reductions
 // are 3-step butterflies inside the group (xor 4, 2, 1), fixed order.
 constexpr int kFinLanes = 8;
+#ifndef HB_FIN_MINB
+#define HB_FIN_MINB 8
+#endif
 
 __device__ __forceinline__ void group_argmax_sum(double &best, int &bidx, double &sum) {
 #pragma unroll
@@ -1104,7 +1114,7 @@ __device__ __forceinline__ void tile_stats(const double *rec, int ntiles, long l
 
 // row finalize: column pivot (hmatrix.py:329-332) or vanishing row (334-338)
 template <typename T, bool C>
-__global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int n) {
+__global__ void __launch_bounds__(kThreads, HB_FIN_MINB) k_fin_row(AcaDev S, int n) {
   using N = Num<T, C>;
   using V = typename N::V;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1158,7 +1168,7 @@ __global__ void __launch_bounds__(kThreads) k_fin_row(AcaDev S, int n) {
 // column finalize: stopping test (343-357), Frobenius update with the cross
 // terms (359-362), next row pivot (301-314)
 template <typename T, bool C>
-__global__ void __launch_bounds__(kThreads) k_fin_col(AcaDev S, int n) {
+__global__ void __launch_bounds__(kThreads, HB_FIN_MINB) k_fin_col(AcaDev S, int n) {
   using N = Num<T, C>;
   using V = typename N::V;
   constexpr int NC = N::NC;
@@ -1317,7 +1327,7 @@ int aca_select(const Prob<T> &, AcaDev &S, const PhaseArgs &A, cudaStream_t st) 
   Need *bsum = reinterpret_cast<Need *>(A.cub_tmp);
   k_need<NC><<<nb, kNeedThreads, 0, st>>>(S, na, A.col_phase, A.nt, A.ns, bsum);
   HB_CUDA(cudaGetLastError());
-  k_need_blocks<<<1, 1024, 0, st>>>(bsum, nb);
+  k_need_blocks<<<1, 1024, 0, st>>>(bsum, nb, S.nlist);
   HB_CUDA(cudaGetLastError());
   if (nb > 1) k_need_carry<<<nb - 1, kNeedThreads, 0, st>>>(S, na, bsum);
   HB_CUDA(cudaGetLastError());

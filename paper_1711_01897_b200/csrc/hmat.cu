@@ -1166,7 +1166,10 @@ int run_phase(hbem_hmat *H, const Prob<T> &P, int col, long long &pool_top, int 
   S.list = col ? H->listC : H->listA;
   S.nlist = H->d_cnt;
   HB_CHECK((aca_select<T, C>(P, S, A, st)));
-  HB_CHECK(H->read_mail(st, {{&H->mail->tot, S.scan + (H->na - 1), sizeof(Need)},
+  // grand total of the needs: k_need_blocks leaves it behind the block totals
+  const Need *need_tot =
+      reinterpret_cast<const Need *>(H->cub_tmp) + (H->na + kNeedThreads - 1) / kNeedThreads;
+  HB_CHECK(H->read_mail(st, {{&H->mail->tot, need_tot, sizeof(Need)},
                              {&H->mail->n, H->d_cnt, sizeof(int)}}));
   const Need tot = H->mail->tot;
   const int n = H->mail->n;

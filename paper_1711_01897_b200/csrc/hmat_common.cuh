@@ -406,6 +406,7 @@ enum : int { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_FALLBACK = 2, ST_OVERFLOW = 3 }
 
 constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
+constexpr int kNeedThreads = 256;  // k_need block size (block-scan width)
 constexpr long long kPoolSlack = 64;  // factor-pool values kept mapped past the last record
 constexpr int kFinRegs = 8;  // terms gathered per job by k_jobs and held in registers by k_fin
 

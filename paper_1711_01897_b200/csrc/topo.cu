@@ -116,15 +116,23 @@ __global__ void k_pair_fill(int m, const int *ptr, const int *idx, int sym, cons
 __global__ void k_pair_kind(const int4 *elem, const int4 *pairs, long long n,
                             unsigned char *key, unsigned long long *cnt) {
   const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (q >= n) return;
-  const int4 pr = pairs[q];
-  const int4 a = elem[pr.x], b = elem[pr.y];
-  const int ta[3] = {a.x, a.y, a.z};
-  int ns = 0;
+  int ns = -1;
+  if (q < n) {
+    const int4 pr = pairs[q];
+    const int4 a = elem[pr.x], b = elem[pr.y];
+    const int ta[3] = {a.x, a.y, a.z};
+    ns = 0;
 #pragma unroll
-  for (int i = 0; i < 3; ++i) ns += (ta[i] == b.x || ta[i] == b.y || ta[i] == b.z) ? 1 : 0;
-  key[q] = (unsigned char)ns;
-  atomicAdd(cnt + ns, 1ull);
+    for (int i = 0; i < 3; ++i) ns += (ta[i] == b.x || ta[i] == b.y || ta[i] == b.z) ? 1 : 0;
+    key[q] = (unsigned char)ns;
+  }
+  // warp-aggregated counts (one atomic per class per warp)
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const unsigned m = __ballot_sync(0xffffffffu, ns == c);
+    if (lane == 0 && m) atomicAdd(cnt + c, (unsigned long long)__popc(m));
+  }
 }
 
 template <typename X> int alloc(std::vector<void *> &allocs, X **p, size_t n) {

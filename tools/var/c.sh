@@ -1,2 +1,2 @@
-HBEM_LIB=var/lib_w1.so timeout 900 python -m pytest tests/test_gpu_c3.py tests/test_gpu_hmatrix.py -q -x 2>&1 | tail -2
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
 bash tools/var/cmp.sh
