@@ -427,12 +427,20 @@ template <typename T, bool C, bool COL, int KK>
 __device__ __forceinline__ void aca_epi_p0(const AcaDev &S, const JobS &J, const V_t<T, C> *cs,
                                            const V_t<T, C> (&f)[kFinRegs], V_t<T, C> *out,
                                            double *rec, int t, int lane, bool valid,
-                                           V_t<T, C> val, double *red) {
+                                           V_t<T, C> val, double *red
+#if HB_PROF
+                                           , unsigned long long *pc, unsigned long long &pt
+#endif
+                                           ) {
   using N = Num<T, C>;
   using V = typename N::V;
   constexpr int NC = N::NC;
 #pragma unroll
   for (int l = 0; l < KK; ++l) val = N::fms(val, cs[l], f[l]);
+#if HB_PROF
+  if ((double)N::re(val) == 1.2345e300) ++pc[0];
+  { const unsigned long long c = clock64(); pc[5] += c - pt; pt = c; }
+#endif
   const int k = J.k;
   if (k > KK) {
     // terms beyond the register batch (late waves of high-rank blocks)
@@ -460,6 +468,10 @@ __device__ __forceinline__ void aca_epi_p0(const AcaDev &S, const JobS &J, const
     rec[0] = cand ? __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml)) : -1.0;
     rec[1] = cand ? (double)(t * 32 + __ffs(cand) - 1) : 2147483647.0;
   }
+#if HB_PROF
+  if (cand == 0x12345u) ++pc[0];
+  { const unsigned long long c = clock64(); pc[7] += c - pt; pt = c; }
+#endif
   // sum |val|^2 and the register-batch dots, one transposed reduction
   constexpr int NV = 1 + KK * NC;
   double v[NV];
@@ -669,6 +681,9 @@ __device__ __forceinline__ void p0_quad(const RuleTab<T> &R, const FixRec<T> *co
 #define HB_ACA_WPC 1
 #endif
 constexpr int kP0Warps = HB_ACA_WPC;
+#ifndef HB_PROF
+#define HB_PROF 0  // per-phase clock64 accounting of k_aca_p0 (timing experiments)
+#endif
 
 template <typename T, bool C, int OP, bool HELM, bool COL>
 __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) k_aca_p0(Prob<T> P, AcaDev S, int n,
@@ -688,6 +703,17 @@ __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long item = (long long)blockIdx.x * kP0Warps + wid;
   if (item >= n_items) return;
+#if HB_PROF
+  unsigned long long pt0 = clock64(), pt = pt0, pc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#define HB_TICK(i)                      \
+  {                                     \
+    const unsigned long long c = clock64(); \
+    pc[i] += c - pt;                    \
+    pt = c;                             \
+  }
+#else
+#define HB_TICK(i)
+#endif
   const int2 it = S.items[item];
   const int p0 = it.x, t = it.y;
   const Job J0 = S.jobs[p0];
@@ -721,6 +747,7 @@ __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) 
   }
   unsigned long long nent = 0, nsing = 0;
   double *red = sred[wid];
+  HB_TICK(1)
   for (int seg = p0;; seg += kSeg) {
     bool ok = false;
     if (lane < kSeg) {
@@ -750,6 +777,7 @@ __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) 
     const unsigned okm = __ballot_sync(kFull, ok) | ~((1u << kSeg) - 1u);
     const int nseg = okm == kFull ? kSeg : __ffs(~okm) - 1;
     __syncwarp();
+    HB_TICK(2)
     for (int q = 0; q < nseg; ++q) {
       const JobS &J = sj[wid][q];
       const int kk = min(J.k, kFinRegs);
@@ -762,6 +790,7 @@ __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) 
         const V *src = sfp[wid][q][use ? l : 0];
         f[l] = use ? ld_ro(src + lane) : N::zero();
       }
+      HB_TICK(8)
       V val;
       {
         const FixRec<T> *const F1[1] = {&sr[wid][q]};
@@ -769,6 +798,10 @@ __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) 
         p0_quad<T, C, OP, HELM, !COL, 1>(P.R, F1, y, ny, nl, v1);
         val = v1[0];
       }
+#if HB_PROF
+      if ((double)N::re(val) == 1.2345e300) ++pc[0];  // the tick below waits for the quadrature
+#endif
+      HB_TICK(3)
       {
         const int4 fev = sr[wid][q].ev;
         unsigned tm = __ballot_sync(kFull, valid && touching4(myev, fev));
@@ -781,25 +814,53 @@ __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) 
           ++nsing;
         }
       }
+      HB_TICK(4)
 #define HB_EPI(KK)                                                                             \
   case KK:                                                                                     \
     aca_epi_p0<T, C, COL, KK>(S, J, sjc[wid][q], f, sout[wid][q], srec[wid][q], t, lane, valid, \
-                              val, red);                                                       \
+                              val, red HB_PROF_ARGS);                                          \
     break;
+#if HB_PROF
+#define HB_PROF_ARGS , pc, pt
+#else
+#define HB_PROF_ARGS
+#endif
       switch (kk) {
         HB_EPI(0) HB_EPI(1) HB_EPI(2) HB_EPI(3) HB_EPI(4) HB_EPI(5) HB_EPI(6) HB_EPI(7) HB_EPI(8)
       }
 #undef HB_EPI
+#undef HB_PROF_ARGS
+      HB_TICK(9)
+#if HB_PROF
+      ++pc[6];
+#endif
     }
     nent += valid ? nseg : 0;
     __syncwarp();
     if (nseg < kSeg) break;
+    HB_TICK(1)
   }
   nent = (unsigned long long)__reduce_add_sync(kFull, (unsigned)nent);
   if (lane == 0) {
     atomicAdd(S.stat, nent);
     if (nsing) atomicAdd(S.stat + 1, nsing);
   }
+#if HB_PROF
+  if (lane == 0) {
+    atomicAdd(S.stat + 4, clock64() - pt0);
+    atomicAdd(S.stat + 5, pc[1]);  // prologue (+ segment turnover)
+    atomicAdd(S.stat + 6, pc[2]);  // staging
+    atomicAdd(S.stat + 12, pc[8]); // factor loads issue
+    atomicAdd(S.stat + 7, pc[3]);  // quadrature
+    atomicAdd(S.stat + 8, pc[4]);  // touching check
+    atomicAdd(S.stat + 9, pc[5]);  // epilogue: residual (waits for the factors)
+    atomicAdd(S.stat + 13, pc[7]); // epilogue: store + pivot candidate
+    atomicAdd(S.stat + 14, pc[9]); // epilogue: sums + records
+    atomicAdd(S.stat + 10, pc[6]); // jobs
+    atomicAdd(S.stat + 11, 1ull);  // warps
+  }
+#endif
+#undef HB_TICK
 }
 
 // ---------------------------------------------------------------------------

@@ -926,7 +926,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   HB_CHECK(dalloc(H, (char **)&S.jc, (size_t)na * kFinRegs * H->vbytes));
   HB_CHECK(dalloc(H, &S.items, H->items_cap));
   if (H->use_erows) HB_CHECK(dalloc(H, &S.eitems, H->eitems_cap));
-  HB_CHECK(dalloc(H, &S.stat, 4));
+  HB_CHECK(dalloc(H, &S.stat, 16));  // [0..1] counters, [4..] HB_PROF phase cycles
   H->cub_bytes = aca_cub_bytes(na);
   HB_CHECK(dalloc(H, (char **)&H->cub_tmp, H->cub_bytes));
   HB_CUDA(cudaMallocHost(&H->mail, sizeof(hbem_hmat::Mail)));
@@ -1377,7 +1377,7 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
                             cudaMemcpyDeviceToHost, H->cpd));
   }
   // ---- ACA waves ------------------------------------------------------------------
-  HB_CUDA(cudaMemsetAsync(S.stat, 0, 32, st));
+  HB_CUDA(cudaMemsetAsync(S.stat, 0, 128, st));
   int waves = 0;
   long long pool_top = 0;
   // HBEM_TRACE: per-wave timeline (host clock, copy-stream completion)
@@ -1616,6 +1616,17 @@ template <typename T, bool C> int execute_t(hbem_hmat *H, cudaStream_t st) {
   HB_CUDA(cudaMemcpyAsync(nf_stat, H->D.stat, 16, cudaMemcpyDeviceToHost, st));
   HB_CUDA(cudaMemcpyAsync(aca_stat, S.stat, 16, cudaMemcpyDeviceToHost, st));
   HB_CUDA(cudaStreamSynchronize(st));
+  if (std::getenv("HBEM_PROF")) {  // phase cycles of a -DHB_PROF=1 kernel build
+    unsigned long long pc[16];
+    HB_CUDA(cudaMemcpy(pc, S.stat, sizeof(pc), cudaMemcpyDeviceToHost));
+    if (pc[10] > 0)
+    std::fprintf(stderr, "[hbem prof] warps %llu jobs %llu | cycles/job: life %.0f prologue %.0f "
+                 "stage %.0f fload %.0f quad %.0f sing %.0f epi: resid %.0f argmax %.0f sums %.0f\n",
+                 pc[11], pc[10], (double)pc[4] / pc[10], (double)pc[5] / pc[10],
+                 (double)pc[6] / pc[10], (double)pc[12] / pc[10], (double)pc[7] / pc[10],
+                 (double)pc[8] / pc[10], (double)pc[9] / pc[10], (double)pc[13] / pc[10],
+                 (double)pc[14] / pc[10]);
+  }
   const auto t_end = clk::now();
   if (wtrace) {
     for (size_t i = 0; i < wcp.size(); ++i) {
