@@ -141,7 +141,15 @@ static __global__ void k_need_carry(AcaDev S, int na, const Need *bsum) {
 }
 
 template <typename T, bool C>
-__global__ void k_jobs(AcaDev S, int n, int col) {
+__device__ void write_stage(const Prob<T> &P, const AcaDev &S, int p, const Job &J,
+                            const long long (&jt)[kFinRegs], const V_t<T, C> (&jc)[kFinRegs],
+                            int col, int local);
+
+// job records, residual terms and warp items of a phase; P0 (stage >= 0):
+// also the job's StageRec (everything k_aca_p0 stages, fixed element relative
+// to the group origin: stage = 1 local frame) and each item's group length
+template <typename T, bool C>
+__global__ void k_jobs(Prob<T> P, AcaDev S, int n, int col, int stage) {
   using N = Num<T, C>;
   using V = typename N::V;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -179,12 +187,19 @@ __global__ void k_jobs(AcaDev S, int n, int col) {
   }
   S.jobs[p] = J;
   // first terms of the residual: record offsets and coefficients
+  long long jt[kFinRegs];
+  V jc[kFinRegs];
+#pragma unroll
+  for (int l = 0; l < kFinRegs; ++l) {
+    jt[l] = 0;
+    jc[l] = N::zero();
+  }
   if (J.k > 0) {
     const V *pool = static_cast<const V *>(S.pool);
     const long long *tl = S.terms + (long long)b * S.tmax;
     const int fixo = col ? J.h + J.fix : J.fix;
-    long long *jt = S.jt + (long long)p * kFinRegs;
-    V *jc = static_cast<V *>(S.jc) + (long long)p * kFinRegs;
+    long long *gjt = S.jt + (long long)p * kFinRegs;
+    V *gjc = static_cast<V *>(S.jc) + (long long)p * kFinRegs;
     const int kk = min(J.k, kFinRegs);
 #pragma unroll
     for (int l = 0; l < kFinRegs; ++l)
@@ -192,11 +207,24 @@ __global__ void k_jobs(AcaDev S, int n, int col) {
         const long long t = tl[l];
         jt[l] = t;
         jc[l] = N::div(pool[t + fixo], pool[t + J.h + J.w]);
+        gjt[l] = jt[l];
+        gjc[l] = jc[l];
       }
   }
+  if (stage >= 0) write_stage<T, C>(P, S, p, J, jt, jc, col, stage);
   if (nd.items) {
     const long long base = sc.items - nd.items;
-    for (long long t = 0; t < nd.items; ++t) S.items[base + t] = make_int2(p, (int)t);
+    // jobs of the group (consecutive positions with this key)
+    int glen = 1;
+    while (p + glen < n) {
+      const int bb = S.list[p + glen];
+      if ((col ? S.rnode[bb] : S.cnode[bb]) != J.key) break;
+      ++glen;
+    }
+    for (long long t = 0; t < nd.items; ++t) {
+      S.items[base + t] = make_int4(p, (int)t, J.vstart, J.nvar);
+      S.iglen[base + t] = glen;
+    }
   }
   if (nd.eitems) {
     const long long base = sc.eitems - nd.eitems;
@@ -269,6 +297,7 @@ __device__ __forceinline__ void cp_async(void *smem, const void *gmem) {
   else
     asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES));
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
@@ -290,6 +319,7 @@ struct JobS {
   long long part;   // first tile record
   long long rsc_off;  // element-row values (linear spaces)
   int b, h, w, k, fix, cur;
+  long long mofs;   // used-index mask words of the varying side (offset)
   unsigned mw;      // used-index mask word of the varying side at this tile
   int nfix;         // tree position of the fixed DOF (its element record, P0)
 };
@@ -424,7 +454,8 @@ __device__ __forceinline__ double tr_sums(const double (&v)[NV], double *red, in
 }
 
 template <typename T, bool C, bool COL, int KK>
-__device__ __forceinline__ void aca_epi_p0(const AcaDev &S, const JobS &J, const V_t<T, C> *cs,
+__device__ __forceinline__ void aca_epi_p0(const AcaDev &S, const JobS &J, unsigned mw,
+                                           const V_t<T, C> *cs,
                                            const V_t<T, C> (&f)[kFinRegs], V_t<T, C> *out,
                                            double *rec, int t, int lane, bool valid,
                                            V_t<T, C> val, double *red
@@ -457,7 +488,7 @@ __device__ __forceinline__ void aca_epi_p0(const AcaDev &S, const JobS &J, const
   }
   if (valid) out[lane] = val;
   // pivot candidate of the tile
-  const bool masked = !valid || ((J.mw >> lane) & 1u) || (COL && t * 32 + lane == J.cur);
+  const bool masked = !valid || ((mw >> lane) & 1u) || (COL && t * 32 + lane == J.cur);
   const unsigned long long bits =
       masked ? 0ull : (unsigned long long)__double_as_longlong(N::abs(val));
   const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
@@ -516,6 +547,7 @@ __device__ __forceinline__ bool stage_job(const AcaDev &S, int p, int n, int key
   js.pe = J.pe;
   js.part = J.part;
   js.rsc_off = J.rsc;
+  js.mofs = J.mofs;
   js.mw = (COL ? S.rmask : S.cmask)[J.mofs + t];
   js.nfix = J.nfix;
   js.b = J.b;
@@ -596,6 +628,55 @@ __device__ __forceinline__ void fix_from_rec(const ElemRec<T> &r, T c0, T c1, T 
   f.ev = r.ev;
 }
 
+// everything k_aca_p0 stages per job, written by k_jobs: one contiguous
+// record per job position, so a warp's segment is a single bulk copy
+template <typename T, bool C> struct alignas(16) StageRec {
+  FixRec<T> f;             // fixed element (local frame: relative to the group origin)
+  JobS j;                  // job view
+  long long jt[kFinRegs];  // pool records of the first terms
+  V_t<T, C> jc[kFinRegs];  // their residual coefficients
+};
+
+template <typename T, bool C>
+__device__ void write_stage(const Prob<T> &P, const AcaDev &S, int p, const Job &J,
+                            const long long (&jt)[kFinRegs], const V_t<T, C> (&jc)[kFinRegs],
+                            int col, int local) {
+  static_assert(sizeof(StageRec<T, C>) <= kStageRecMax, "stage record too large");
+  StageRec<T, C> *o = static_cast<StageRec<T, C> *>(S.stage) + p;
+  JobS js;
+  js.pe = J.pe;
+  js.part = J.part;
+  js.rsc_off = J.rsc;
+  js.mw = 0u;
+  js.nfix = J.nfix;
+  js.b = J.b;
+  js.h = J.h;
+  js.w = J.w;
+  js.k = J.k;
+  js.fix = J.fix;
+  js.cur = J.cur;
+  js.mofs = J.mofs;
+  ElemRec<T> r;
+  load_rec<T>(col ? P.srec : P.trec, J.nfix, r);
+  FixRec<T> f;
+  if (local) {
+    // group origin: the first quadrature point of the varying cluster's first
+    // element (inside the varying cluster, as the local frame requires)
+    ElemRec<T> g;
+    load_rec<T>(col ? P.trec : P.srec, J.vstart, g);
+    fix_from_rec<T, true>(r, g.q[0], g.q[1], g.q[2], f);
+  } else {
+    fix_from_rec<T, false>(r, T(0), T(0), T(0), f);
+  }
+  o->f = f;
+  o->j = js;
+#pragma unroll
+  for (int l = 0; l < kFinRegs; ++l) {
+    o->jt[l] = jt[l];
+    o->jc[l] = jc[l];
+  }
+}
+
 // NJ fixed elements F against the lane's element (points y, local |y'|^2 in
 // ny, normal nl).  FIXED_TEST: the fixed elements are test elements (row
 // jobs); otherwise trial elements (column jobs).
@@ -670,10 +751,12 @@ __device__ __forceinline__ void p0_quad(const RuleTab<T> &R, const FixRec<T> *co
 // ---------------------------------------------------------------------------
 // K3 (P0): one warp per (group head, 32-wide tile).  Lane l keeps the varying
 // element of tile column 32 t + l in registers and walks every job of the
-// group; fixed elements, job views and residual coefficients of kSeg jobs at
-// a time are staged in shared memory and broadcast.  The residual factor
-// values of a job are loaded (cp.async) before its integral so their latency
-// hides behind the quadrature.
+// group.  The group's stage records (fixed element relative to the group
+// origin, job view, residual terms; k_jobs) are copied to shared memory kSeg
+// at a time with cp.async and broadcast, so an item waits for two dependent
+// loads (item -> records and its lane element), not a chain of five.  The
+// residual factor values and the tile's mask word of a job are loaded before
+// its integral so their latency hides behind the quadrature.
 // ---------------------------------------------------------------------------
 // warps per CTA of k_aca_p0: independent warps (their items differ in length)
 // so a CTA's slot frees as soon as its own warps finish
@@ -690,56 +773,65 @@ __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) 
                                                                    long long n_items) {
   using N = Num<T, C>;
   using V = typename N::V;
+  using SR = StageRec<T, C>;
   constexpr int NC = N::NC;
-  constexpr bool LOCAL = P0Local<T, OP>::value;
   constexpr int kSeg = sizeof(V) > 8 ? 8 : 16;  // jobs staged per segment
-  __shared__ FixRec<T> sr[kP0Warps][kSeg];
-  __shared__ JobS sj[kP0Warps][kSeg];
-  __shared__ const V *sfp[kP0Warps][kSeg][kFinRegs];  // factor values of this tile, term l
-  __shared__ V sjc[kP0Warps][kSeg][kFinRegs];         // residual coefficients
-  __shared__ V *sout[kP0Warps][kSeg];                 // this tile of the pending record
-  __shared__ double *srec[kP0Warps][kSeg];            // this tile's record
+  constexpr int kChunks = (int)(sizeof(SR) / 16);
+  __shared__ SR ssr[kP0Warps][kSeg];
   __shared__ double sred[kP0Warps][32 * kRedStride];  // transpose scratch
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long item = (long long)blockIdx.x * kP0Warps + wid;
   if (item >= n_items) return;
 #if HB_PROF
   unsigned long long pt0 = clock64(), pt = pt0, pc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-#define HB_TICK(i)                      \
-  {                                     \
+#define HB_TICK(i)                          \
+  {                                         \
     const unsigned long long c = clock64(); \
-    pc[i] += c - pt;                    \
-    pt = c;                             \
+    pc[i] += c - pt;                        \
+    pt = c;                                 \
   }
+#define HB_PROF_ARGS , pc, pt
 #else
 #define HB_TICK(i)
+#define HB_PROF_ARGS
 #endif
-  const int2 it = S.items[item];
-  const int p0 = it.x, t = it.y;
-  const Job J0 = S.jobs[p0];
-  const int key0 = J0.key, vstart = J0.vstart, nvar = J0.nvar;
+  const int4 it = S.items[item];
+  const int glen = S.iglen[item];
+  const int p0 = it.x, t = it.y, vstart = it.z, nvar = it.w;
   const int idx = t * 32 + lane;
   const bool valid = idx < nvar;
+  const SR *gsr = static_cast<const SR *>(S.stage) + p0;
+  // segment copy: lanes stride over the 16-byte chunks of nj records
+  auto fetch = [&](int seg) {
+    const int nj = min(kSeg, glen - seg);
+    const uint4 *src = reinterpret_cast<const uint4 *>(gsr + seg);
+    uint4 *dst = reinterpret_cast<uint4 *>(&ssr[wid][0]);
+    for (int c = lane; c < nj * kChunks; c += 32) cp_async<16>(dst + c, src + c);
+    cp_async_commit();
+  };
+  fetch(0);
   T y[18], ny[6], nl[4];
   int4 myev;
-  T c0 = T(0), c1 = T(0), c2 = T(0);
   {
     ElemRec<T> my;
     load_rec<T>(COL ? P.trec : P.srec, vstart + (valid ? idx : nvar - 1), my);
-    if (LOCAL) {
-      // warp-uniform origin: lane 0's first quadrature point (idx 0 of the
-      // tile is always valid)
-      c0 = __shfl_sync(kFull, my.q[0], 0);
-      c1 = __shfl_sync(kFull, my.q[1], 0);
-      c2 = __shfl_sync(kFull, my.q[2], 0);
+    T c0 = T(0), c1 = T(0), c2 = T(0);
+    if (P0Local<T, OP>::value) {
+      // group origin (k_jobs, write_stage): the varying cluster's first
+      // element's first quadrature point
+      const T *g = (COL ? P.trec : P.srec) + (size_t)vstart * (sizeof(T) == 8 ? 24 : 28);
+      c0 = __ldg(g);
+      c1 = __ldg(g + 1);
+      c2 = __ldg(g + 2);
     }
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
       y[3 * i] = my.q[3 * i] - c0;
       y[3 * i + 1] = my.q[3 * i + 1] - c1;
       y[3 * i + 2] = my.q[3 * i + 2] - c2;
-      ny[i] = LOCAL ? y[3 * i] * y[3 * i] + y[3 * i + 1] * y[3 * i + 1] + y[3 * i + 2] * y[3 * i + 2]
-                    : T(0);
+      ny[i] = P0Local<T, OP>::value
+                  ? y[3 * i] * y[3 * i] + y[3 * i + 1] * y[3 * i + 1] + y[3 * i + 2] * y[3 * i + 2]
+                  : T(0);
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) nl[c] = my.n[c];
@@ -747,53 +839,37 @@ __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) 
   }
   unsigned long long nent = 0, nsing = 0;
   double *red = sred[wid];
+  V *const pool = static_cast<V *>(S.pool);
+  const unsigned *mask = COL ? S.rmask : S.cmask;
+  const int to = t * 32;
   HB_TICK(1)
-  for (int seg = p0;; seg += kSeg) {
-    bool ok = false;
-    if (lane < kSeg) {
-      JobS js;
-      long long jt[kFinRegs];
-      V jc[kFinRegs];
-      ok = stage_job<T, C, COL>(S, seg + lane, n, key0, t, js, jt, jc);
-      if (ok) {
-        sj[wid][lane] = js;
-        V *pool = static_cast<V *>(S.pool);
-        const int ro = COL ? 0 : js.h;
-#pragma unroll
-        for (int l = 0; l < kFinRegs; ++l)
-          if (l < min(js.k, kFinRegs)) {
-            sfp[wid][lane][l] = pool + jt[l] + ro + t * 32;
-            sjc[wid][lane][l] = jc[l];
-          }
-        sout[wid][lane] = pool + js.pe + (COL ? 0 : js.h) + t * 32;
-        srec[wid][lane] = S.part + js.part + (long long)t * part_len(js.k, NC);
-        ElemRec<T> r;
-        load_rec<T>(COL ? P.srec : P.trec, js.nfix, r);
-        FixRec<T> f;
-        fix_from_rec<T, LOCAL>(r, c0, c1, c2, f);
-        sr[wid][lane] = f;
-      }
+  for (int seg = 0; seg < glen; seg += kSeg) {
+    if (seg > 0) {
+      __syncwarp();  // the previous segment's records are no longer read
+      fetch(seg);
     }
-    const unsigned okm = __ballot_sync(kFull, ok) | ~((1u << kSeg) - 1u);
-    const int nseg = okm == kFull ? kSeg : __ffs(~okm) - 1;
+    cp_async_wait_all();
     __syncwarp();
+    const int nseg = min(kSeg, glen - seg);
     HB_TICK(2)
     for (int q = 0; q < nseg; ++q) {
-      const JobS &J = sj[wid][q];
+      const SR &R = ssr[wid][q];
+      const JobS &J = R.j;
       const int kk = min(J.k, kFinRegs);
-      // factor values of the residual, loaded before the quadrature so their
-      // latency hides behind it (predicated loads, no branches)
+      const int ro = COL ? 0 : J.h;
+      // factor values of the residual and the tile's mask word, loaded before
+      // the quadrature so their latency hides behind it (predicated loads)
+      const unsigned mw = __ldg(mask + J.mofs + t);
       V f[kFinRegs];
 #pragma unroll
       for (int l = 0; l < kFinRegs; ++l) {
         const bool use = l < kk && valid;
-        const V *src = sfp[wid][q][use ? l : 0];
-        f[l] = use ? ld_ro(src + lane) : N::zero();
+        f[l] = use ? ld_ro(pool + R.jt[l] + ro + to + lane) : N::zero();
       }
       HB_TICK(8)
       V val;
       {
-        const FixRec<T> *const F1[1] = {&sr[wid][q]};
+        const FixRec<T> *const F1[1] = {&R.f};
         V v1[1];
         p0_quad<T, C, OP, HELM, !COL, 1>(P.R, F1, y, ny, nl, v1);
         val = v1[0];
@@ -803,7 +879,7 @@ __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) 
 #endif
       HB_TICK(3)
       {
-        const int4 fev = sr[wid][q].ev;
+        const int4 fev = R.f.ev;
         unsigned tm = __ballot_sync(kFull, valid && touching4(myev, fev));
         while (tm) {
           const int src = __ffs(tm) - 1;
@@ -815,29 +891,23 @@ __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) 
         }
       }
       HB_TICK(4)
+      V *const out = pool + J.pe + ro + to;
+      double *const rec = S.part + J.part + (long long)t * part_len(J.k, NC);
 #define HB_EPI(KK)                                                                             \
   case KK:                                                                                     \
-    aca_epi_p0<T, C, COL, KK>(S, J, sjc[wid][q], f, sout[wid][q], srec[wid][q], t, lane, valid, \
-                              val, red HB_PROF_ARGS);                                          \
+    aca_epi_p0<T, C, COL, KK>(S, J, mw, R.jc, f, out, rec, t, lane, valid, val,                \
+                              red HB_PROF_ARGS);                                               \
     break;
-#if HB_PROF
-#define HB_PROF_ARGS , pc, pt
-#else
-#define HB_PROF_ARGS
-#endif
       switch (kk) {
         HB_EPI(0) HB_EPI(1) HB_EPI(2) HB_EPI(3) HB_EPI(4) HB_EPI(5) HB_EPI(6) HB_EPI(7) HB_EPI(8)
       }
 #undef HB_EPI
-#undef HB_PROF_ARGS
       HB_TICK(9)
 #if HB_PROF
       ++pc[6];
 #endif
     }
     nent += valid ? nseg : 0;
-    __syncwarp();
-    if (nseg < kSeg) break;
     HB_TICK(1)
   }
   nent = (unsigned long long)__reduce_add_sync(kFull, (unsigned)nent);
@@ -861,6 +931,7 @@ __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) 
   }
 #endif
 #undef HB_TICK
+#undef HB_PROF_ARGS
 }
 
 // ---------------------------------------------------------------------------
@@ -1011,7 +1082,7 @@ __global__ void __launch_bounds__(kThreads) k_aca_gen(Prob<T> P, AcaDev S, int n
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long item = (long long)blockIdx.x * kWarps + wid;
   if (item >= n_items) return;
-  const int2 it = S.items[item];
+  const int4 it = S.items[item];
   const int p0 = it.x, t = it.y;
   const Job J0 = S.jobs[p0];
   const int key0 = J0.key;
@@ -1408,7 +1479,8 @@ int aca_phase(const Prob<T> &P, AcaDev &S, const PhaseArgs &A, int op, bool helm
               int n, long long n_items, long long n_eitems, cudaStream_t st) {
   if (n <= 0) return HBEM_OK;
   const int col = A.col_phase;
-  k_jobs<T, C><<<(n + 127) / 128, 128, 0, st>>>(S, n, col);
+  const int stage = (nt == 1 && ns == 1) ? (std::is_same<T, double>::value && op == HBEM_SLP ? 1 : 0) : -1;
+  k_jobs<T, C><<<(n + 127) / 128, 128, 0, st>>>(P, S, n, col, stage);
   HB_CUDA(cudaGetLastError());
   if (S.rsc && n_eitems > 0) {
     // linear spaces: element rows first, then the DOF gather + residual

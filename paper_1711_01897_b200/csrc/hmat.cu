@@ -925,6 +925,8 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   HB_CHECK(dalloc(H, &S.jt, (size_t)na * kFinRegs));
   HB_CHECK(dalloc(H, (char **)&S.jc, (size_t)na * kFinRegs * H->vbytes));
   HB_CHECK(dalloc(H, &S.items, H->items_cap));
+  HB_CHECK(dalloc(H, &S.iglen, H->items_cap));
+  if (H->p0) HB_CHECK(dalloc(H, (char **)&S.stage, (size_t)na * kStageRecMax));
   if (H->use_erows) HB_CHECK(dalloc(H, &S.eitems, H->eitems_cap));
   HB_CHECK(dalloc(H, &S.stat, 16));  // [0..1] counters, [4..] HB_PROF phase cycles
   H->cub_bytes = aca_cub_bytes(na);

@@ -407,6 +407,7 @@ enum : int { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_FALLBACK = 2, ST_OVERFLOW = 3 }
 constexpr int kThreads = 128;
 constexpr int kWarps = kThreads / 32;
 constexpr int kNeedThreads = 256;  // k_need block size (block-scan width)
+constexpr size_t kStageRecMax = 512;  // bytes per job of the P0 stage records (StageRec)
 constexpr long long kPoolSlack = 64;  // factor-pool values kept mapped past the last record
 constexpr int kFinRegs = 8;  // terms gathered per job by k_jobs and held in registers by k_fin
 
@@ -474,7 +475,9 @@ struct AcaDev {
   const int *nlist;  // device count of list
   Need *need, *scan;
   Job *jobs;
-  int2 *items;       // (head position, tile)
+  int4 *items;       // (head position, tile, varying start, varying length)
+  int *iglen;        // per item: jobs in its group
+  void *stage;       // P0: per job position, its StageRec (k_jobs -> k_aca_p0)
   int2 *eitems;      // linear spaces: (head position, element tile)
   void *rsc;         // linear spaces: element-row values of the current phase
   // linear spaces: per cluster node, the sorted union of the elements that
