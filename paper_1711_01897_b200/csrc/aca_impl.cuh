@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(kNeedThreads) k_need(AcaDev S, int na, int col
     const int h = S.h[b], w = S.w[b], k = S.rank[b];
     const int tiles = tiles_of(col ? h : w);
     const int key = col ? S.rnode[b] : S.cnode[b];
+    S.pkey[p] = key;
     bool head = p == 0;
     if (!head) {
       const int bp = S.list[p - 1];
@@ -148,8 +149,11 @@ __device__ void write_stage(const Prob<T> &P, const AcaDev &S, int p, const Job 
 // job records, residual terms and warp items of a phase; P0 (stage >= 0):
 // also the job's StageRec (everything k_aca_p0 stages, fixed element relative
 // to the group origin: stage = 1 local frame) and each item's group length
+#ifndef HB_JOBS_MINB
+#define HB_JOBS_MINB 1
+#endif
 template <typename T, bool C>
-__global__ void k_jobs(Prob<T> P, AcaDev S, int n, int col, int stage) {
+__global__ void __launch_bounds__(128, HB_JOBS_MINB) k_jobs(Prob<T> P, AcaDev S, int n, int col, int stage) {
   using N = Num<T, C>;
   using V = typename N::V;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -216,11 +220,7 @@ __global__ void k_jobs(Prob<T> P, AcaDev S, int n, int col, int stage) {
     const long long base = sc.items - nd.items;
     // jobs of the group (consecutive positions with this key)
     int glen = 1;
-    while (p + glen < n) {
-      const int bb = S.list[p + glen];
-      if ((col ? S.rnode[bb] : S.cnode[bb]) != J.key) break;
-      ++glen;
-    }
+    while (p + glen < n && S.pkey[p + glen] == J.key) ++glen;
     for (long long t = 0; t < nd.items; ++t) {
       S.items[base + t] = make_int4(p, (int)t, J.vstart, J.nvar);
       S.iglen[base + t] = glen;
@@ -662,9 +662,8 @@ __device__ void write_stage(const Prob<T> &P, const AcaDev &S, int p, const Job 
   if (local) {
     // group origin: the first quadrature point of the varying cluster's first
     // element (inside the varying cluster, as the local frame requires)
-    ElemRec<T> g;
-    load_rec<T>(col ? P.trec : P.srec, J.vstart, g);
-    fix_from_rec<T, true>(r, g.q[0], g.q[1], g.q[2], f);
+    const T *g = (col ? P.trec : P.srec) + (size_t)J.vstart * (sizeof(T) == 8 ? 24 : 28);
+    fix_from_rec<T, true>(r, __ldg(g), __ldg(g + 1), __ldg(g + 2), f);
   } else {
     fix_from_rec<T, false>(r, T(0), T(0), T(0), f);
   }

@@ -920,6 +920,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   HB_CHECK(dalloc(H, &H->listC, na));
   HB_CHECK(dalloc(H, &H->d_cnt, 1));
   HB_CHECK(dalloc(H, &S.need, na));
+  HB_CHECK(dalloc(H, &S.pkey, na));
   HB_CHECK(dalloc(H, &S.scan, na));
   HB_CHECK(dalloc(H, &S.jobs, na));
   HB_CHECK(dalloc(H, &S.jt, (size_t)na * kFinRegs));

@@ -474,6 +474,7 @@ struct AcaDev {
   const int *list;   // positions -> block (sorted by key)
   const int *nlist;  // device count of list
   Need *need, *scan;
+  int *pkey;         // per list position: the grouping key (k_need)
   Job *jobs;
   int4 *items;       // (head position, tile, varying start, varying length)
   int *iglen;        // per item: jobs in its group
