@@ -201,19 +201,26 @@ __global__ void __launch_bounds__(128, HB_JOBS_MINB) k_jobs(Prob<T> P, AcaDev S,
   if (J.k > 0) {
     const V *pool = static_cast<const V *>(S.pool);
     const long long *tl = S.terms + (long long)b * S.tmax;
+    const V *tp = static_cast<const V *>(S.tpiv) + (long long)b * S.tmax;
     const int fixo = col ? J.h + J.fix : J.fix;
-    long long *gjt = S.jt + (long long)p * kFinRegs;
-    V *gjc = static_cast<V *>(S.jc) + (long long)p * kFinRegs;
     const int kk = min(J.k, kFinRegs);
 #pragma unroll
     for (int l = 0; l < kFinRegs; ++l)
       if (l < kk) {
         const long long t = tl[l];
         jt[l] = t;
-        jc[l] = N::div(pool[t + fixo], pool[t + J.h + J.w]);
-        gjt[l] = jt[l];
-        gjc[l] = jc[l];
+        jc[l] = N::div(pool[t + fixo], tp[l]);
       }
+    if (stage < 0) {  // the linear-space kernels read them from here
+      long long *gjt = S.jt + (long long)p * kFinRegs;
+      V *gjc = static_cast<V *>(S.jc) + (long long)p * kFinRegs;
+#pragma unroll
+      for (int l = 0; l < kFinRegs; ++l)
+        if (l < kk) {
+          gjt[l] = jt[l];
+          gjc[l] = jc[l];
+        }
+    }
   }
   if (stage >= 0) write_stage<T, C>(P, S, p, J, jt, jc, col, stage);
   if (nd.items) {
@@ -1360,7 +1367,7 @@ __global__ void __launch_bounds__(kThreads, HB_FIN_MINB) k_fin_col(AcaDev S, int
           if (C) vi += rd[t * ps + (long long)l * NC + 1];
         }
       }
-      const V pl = pool[tl[l] + h + w];
+      const V pl = static_cast<const V *>(S.tpiv)[(long long)b * S.tmax + l];
       const double plr = (double)N::re(pl), pli = (double)N::im(pl);
       const double dr = plr * pr + pli * pim, di = plr * pim - pli * pr;  // conj(p_l) p
       double qr, qi;
@@ -1401,6 +1408,8 @@ __global__ void __launch_bounds__(kThreads, HB_FIN_MINB) k_fin_col(AcaDev S, int
   S.norm2[b] = n2n;
   S.small[b] = 0;
   S.terms[(long long)b * S.tmax + k] = J.pe;
+  // the term's pivot (= its record's last value) next to the term list
+  static_cast<V *>(S.tpiv)[(long long)b * S.tmax + k] = N::mk((T)pr, (T)pim);
   S.pend[b] = -1;
   S.rank[b] = k + 1;
   set_bit(rm, i);

@@ -911,6 +911,7 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
   HB_CHECK(dalloc(H, &S.rowpart, na));
   HB_CHECK(dalloc(H, &S.rsum, (size_t)na * kFinRegs * 2));
   HB_CHECK(dalloc(H, &S.terms, (size_t)na * S.tmax));
+  HB_CHECK(dalloc(H, (char **)&S.tpiv, (size_t)na * S.tmax * H->vbytes));
   HB_CHECK(dalloc(H, &S.rmask, rmw));
   HB_CHECK(dalloc(H, &S.cmask, cmw));
   HB_CHECK(dalloc(H, &S.flagA, na));

@@ -486,6 +486,7 @@ struct AcaDev {
   const long long *recl_ptr, *cecl_ptr;
   const int *recl, *cecl;
   double *part;      // dot records of the current phase (k values per job)
+  void *tpiv;        // per block and term: the term's pivot value (V), contiguous per block
   long long *jt;     // per job: record offsets of its first kFinRegs terms
   void *jc;          // per job: their residual coefficients (u_l[i] / p_l or r_l[j] / p_l)
   const double *rpart;  // row-phase partial records (read by the column finalize)
