@@ -500,11 +500,16 @@ __device__ __forceinline__ void aca_epi_p0(const AcaDev &S, const JobS &J, unsig
       masked ? 0ull : (unsigned long long)__double_as_longlong(N::abs(val));
   const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
   const unsigned mh = __reduce_max_sync(kFull, hi);
-  const unsigned ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
-  const unsigned cand = __ballot_sync(kFull, !masked && hi == mh && lo == ml);
-  if (lane == 0) {
-    rec[0] = cand ? __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml)) : -1.0;
-    rec[1] = cand ? (double)(t * 32 + __ffs(cand) - 1) : 2147483647.0;
+  unsigned cand = __ballot_sync(kFull, !masked && hi == mh);
+  if (cand & (cand - 1)) {
+    // several lanes share the maximal high word (rare): compare the low words
+    const unsigned ml = __reduce_max_sync(kFull, ((cand >> lane) & 1u) ? lo : 0u);
+    cand &= __ballot_sync(kFull, lo == ml);
+  }
+  // the winner (first index on ties) writes its own |val|; lane 0 the empty record
+  if (lane == (cand ? __ffs(cand) - 1 : 0)) {
+    rec[0] = cand ? __longlong_as_double((long long)bits) : -1.0;
+    rec[1] = cand ? (double)(t * 32 + lane) : 2147483647.0;
   }
 #if HB_PROF
   if (cand == 0x12345u) ++pc[0];
