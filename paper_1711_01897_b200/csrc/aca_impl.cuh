@@ -877,6 +877,10 @@ __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) 
         const bool use = l < kk && valid;
         f[l] = use ? ld_ro(pool + R.jt[l] + ro + to + lane) : N::zero();
       }
+      // touching pairs (rare; Sauter-Schwab in place), tested before the
+      // quadrature so the test's latency overlaps it
+      const int4 fev = R.f.ev;
+      unsigned tm = __ballot_sync(kFull, valid && touching4(myev, fev));
       HB_TICK(8)
       V val;
       {
@@ -890,8 +894,6 @@ __global__ void __launch_bounds__(kP0Warps * 32, HB_ACA_P0_MINB * 4 / kP0Warps) 
 #endif
       HB_TICK(3)
       {
-        const int4 fev = R.f.ev;
-        unsigned tm = __ballot_sync(kFull, valid && touching4(myev, fev));
         while (tm) {
           const int src = __ffs(tm) - 1;
           tm &= tm - 1;
