@@ -84,14 +84,15 @@ __global__ void __launch_bounds__(kNeedThreads) k_need(AcaDev S, int na, int col
   Need d{0, 0, 0, 0, 0};
   if (p < n && p < na) {
     const int b = S.list[p];
-    const int h = S.h[b], w = S.w[b], k = S.rank[b];
+    const BlockInfo bi = S.binfo[b];
+    const int h = bi.h, w = bi.w, k = S.rank[b];
     const int tiles = tiles_of(col ? h : w);
-    const int key = col ? S.rnode[b] : S.cnode[b];
+    const int key = col ? bi.rnode : bi.cnode;
     S.pkey[p] = key;
     bool head = p == 0;
     if (!head) {
       const int bp = S.list[p - 1];
-      head = key != (col ? S.rnode[bp] : S.cnode[bp]);
+      head = key != (col ? S.binfo[bp].rnode : S.binfo[bp].cnode);
     }
     d.pool = (!col && S.pend[b] < 0) ? (long long)h + w + 1 : 0;
     // per tile: statistics (4) + dots (k NC), padded even (part_len)
@@ -160,31 +161,32 @@ __global__ void __launch_bounds__(128, HB_JOBS_MINB) k_jobs(Prob<T> P, AcaDev S,
   if (p >= n) return;
   const int b = S.list[p];
   const Need sc = S.scan[p], nd = S.need[p];
+  const BlockInfo bi = S.binfo[b];
   Job J;
   J.b = b;
-  J.h = S.h[b];
-  J.w = S.w[b];
+  J.h = bi.h;
+  J.w = bi.w;
   J.k = S.rank[b];
-  const int r0 = S.r0[b], c0 = S.c0[b];
+  const int r0 = bi.r0, c0 = bi.c0;
   J.part = sc.part - nd.part;
   J.rsc = sc.rsc - nd.rsc;
   if (!col) {
-    J.key = S.cnode[b];
+    J.key = bi.cnode;
     J.fix = S.cur[b];
     const long long pe = S.pend[b];
     J.pe = pe >= 0 ? pe : S.pool_base + sc.pool - nd.pool;
     J.nfix = r0 + J.fix;
-    J.mofs = S.cmask_off[b];
+    J.mofs = bi.cmo;
     J.vstart = c0;
     J.nvar = J.w;
     J.cur = J.fix;
     S.rowpart[b] = J.part;
   } else {
-    J.key = S.rnode[b];
+    J.key = bi.rnode;
     J.fix = S.pcol[b];
     J.pe = S.pend[b];
     J.nfix = c0 + J.fix;
-    J.mofs = S.rmask_off[b];
+    J.mofs = bi.rmo;
     J.vstart = r0;
     J.nvar = J.h;
     J.cur = S.cur[b];

@@ -885,6 +885,15 @@ int setup(hbem_hmat *H, const hbem_hmat_desc *d) {
     long long *pl;
     HB_CHECK(upload(H, &pl, rmo)); S.rmask_off = pl;
     HB_CHECK(upload(H, &pl, cmo)); S.cmask_off = pl;
+    {
+      std::vector<BlockInfo> bi((size_t)na);
+      for (int q = 0; q < na; ++q)
+        bi[(size_t)q] = BlockInfo{H->ah[q], H->aw[q], H->ar0[q], H->ac0[q], rnode[q], cnode[q],
+                                  rmo[q], cmo[q]};
+      BlockInfo *pb;
+      HB_CHECK(upload(H, &pb, bi));
+      S.binfo = pb;
+    }
     // static phase orders: row jobs grouped by column cluster, column jobs
     // by row cluster, ties by block index (counting sort: deterministic lists)
     auto by_key = [&](const std::vector<int> &key, int64_t n_keys) {

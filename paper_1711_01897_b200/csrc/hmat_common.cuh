@@ -452,6 +452,13 @@ struct SumNeed {
   }
 };
 
+// static per-block fields in one record: a job's block costs one or two
+// sectors instead of one per field array
+struct BlockInfo {
+  int h, w, r0, c0, rnode, cnode;
+  long long rmo, cmo;  // used-index mask word offsets (rows, columns)
+};
+
 struct AcaDev {
   // static per block
   const int *h, *w, *r0, *c0, *rnode, *cnode;
@@ -465,6 +472,7 @@ struct AcaDev {
   int tmax;
   unsigned *rmask, *cmask;
   const long long *rmask_off, *cmask_off;
+  const struct BlockInfo *binfo;  // the static fields above, one record per block (k_jobs)
   void *pool;
   long long pool_cap, pool_base;
   int kmax_cfg;
